@@ -1,0 +1,210 @@
+/*
+ * ai3.h -- C ABI of libai3.so, the B200 (sm_100a) forward-convolution library
+ * behind the ai3 algorithm-selection hooks (arXiv 2410.08300).
+ *
+ * The operation (every entry point that computes): forward 2-D convolution,
+ *
+ *   y[n][k][p][q] = b[k] + sum_{c', r, s} x[n][g*C/G + c'][p*sh - ph + r*dh][q*sw - pw + s*dw]
+ *                                        * w[k][c'][r][s]
+ *
+ * i.e. cross-correlation with zero padding plus an optional bias, exactly what
+ * torch.nn.Conv2d computes (PAPER.md:138-139, :163, :167 assert equality with
+ * PyTorch; SPEC.md:130 writes the sum out).  Output extents use floor rounding,
+ * P = floor((H + 2ph - dh(R-1) - 1)/sh) + 1.  g = k / (K/G).
+ *
+ * The user selects the ALGORITHM that computes it, per call or per plan
+ * (PAPER.md:104, :142, :170):
+ *   AI3_ALGO_DIRECT         -- direct convolution, no data transform (§II.B(d))
+ *   AI3_ALGO_GEMM           -- explicit IM2COL matrix + GEMM (§II.B(a), :194 §V.B(c))
+ *   AI3_ALGO_IMPLICIT_GEMM  -- GEMM without forming the matrix, zero extra memory (§V.B(b))
+ *   AI3_ALGO_WINOGRAD       -- Winograd minimal filtering F(2x2,3x3) (§V.B(d))
+ *   AI3_ALGO_GUESS          -- shape-based heuristic choice ("guess")
+ * All algorithms compute the same function; they differ in rounding only.
+ *
+ * Conventions (all entry points):
+ *   * Return value: ai3_status.  On any non-OK status nothing was launched and
+ *     ai3_last_error() (thread-local) describes the offending sizes/constraint.
+ *   * Memory ownership: the CALLER owns every buffer (x, w, b, y, workspace,
+ *     plan weight buffer, staging buffers).  The library never allocates device
+ *     memory; plans hold only borrowed pointers and host-side descriptors.
+ *   * Asynchrony: compute calls enqueue kernels on `stream` (a cudaStream_t
+ *     passed as void*, NULL = legacy default stream) and return immediately.
+ *     Device faults surface at the caller's next synchronisation.
+ *   * Threading: plans are immutable after creation except for an internal,
+ *     mutex-protected descriptor cache; concurrent calls on different streams
+ *     are safe.
+ *   * Determinism: for a given plan and input, results are bit-identical run to
+ *     run (no atomics; each output element is reduced in a fixed order that does
+ *     not depend on the batch size).
+ *   * Tensor descriptors: logical NCHW extents (n,c,h,w) for activations; the
+ *     `layout` field says how the contiguous buffer is ordered (NCHW or NHWC =
+ *     torch channels_last).  Weights are always KCRS contiguous (PyTorch order).
+ *     Bias has K elements of the weight's dtype, or is NULL.
+ */
+#ifndef AI3_H
+#define AI3_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AI3_VERSION 1000 /* 0.1.0 */
+
+typedef enum {
+    AI3_OK = 0,
+    AI3_ERR_INVALID_ARGUMENT = 1, /* null pointer, rank/extent < 1, stride/dilation < 1, pad < 0 */
+    AI3_ERR_SHAPE = 2,            /* channel/group mismatch, bad weight/bias/output extents,
+                                     kernel larger than padded input */
+    AI3_ERR_UNSUPPORTED = 3,      /* algorithm precondition violated (e.g. winograd on 5x5,
+                                     stride 2, groups > 1) or dtype/math combo */
+    AI3_ERR_UNKNOWN_ALGORITHM = 4,/* name not in the algorithm set */
+    AI3_ERR_WORKSPACE = 5,        /* workspace / weight buffer / staging too small or misaligned */
+    AI3_ERR_CUDA = 6              /* a CUDA runtime/driver call failed at launch */
+} ai3_status;
+
+typedef enum {
+    AI3_ALGO_GUESS = 0,             /* names "guess", "default", "auto" */
+    AI3_ALGO_DIRECT = 1,            /* "direct" */
+    AI3_ALGO_GEMM = 2,              /* "gemm", "im2col" */
+    AI3_ALGO_IMPLICIT_GEMM = 3,     /* "implicit_gemm" */
+    AI3_ALGO_WINOGRAD = 4,          /* "winograd" */
+    /* reserved names, recognised but AI3_ERR_UNSUPPORTED until built */
+    AI3_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* "implicit_precomp_gemm" */
+    AI3_ALGO_SMM = 6,               /* "smm" */
+    AI3_ALGO_KN2ROW = 7,            /* "kn2row" */
+    AI3_ALGO_CUSTOM = 8             /* "custom" */
+} ai3_algo;
+
+typedef enum { AI3_F32 = 0, AI3_BF16 = 1 } ai3_dtype;
+
+/* Arithmetic for fp32 tensors.  STRICT: fp32-accurate (FFMA, or 3xTF32 split
+ * products on the tensor cores).  TF32: operands rounded to TF32 (nearest) for
+ * the tensor-core algorithms, like torch.backends.cuda.matmul.allow_tf32.
+ * BF16 tensors always multiply bf16 operands with fp32 accumulation. */
+typedef enum { AI3_MATH_STRICT = 0, AI3_MATH_TF32 = 1 } ai3_math;
+
+typedef enum { AI3_NCHW = 0, AI3_NHWC = 1 } ai3_layout;
+
+/* A dense 4-D activation (or KCRS weight) tensor. */
+typedef struct {
+    void* data;                 /* device pointer (host pointer only where stated) */
+    int64_t n, c, h, w;         /* logical NCHW extents (for weights: K, C/G, R, S) */
+    int32_t dtype;              /* ai3_dtype */
+    int32_t layout;             /* ai3_layout; weights must be AI3_NCHW (= KCRS) */
+} ai3_tensor4d;
+
+/* Convolution hyperparameters (nn.Conv2d's). */
+typedef struct {
+    int64_t out_channels;       /* K */
+    int32_t kernel[2];          /* R, S */
+    int32_t stride[2];          /* sh, sw >= 1 */
+    int32_t padding[2];         /* ph, pw >= 0 (symmetric zero padding) */
+    int32_t dilation[2];        /* dh, dw >= 1 */
+    int32_t groups;             /* G >= 1, divides C and K */
+    int32_t has_bias;           /* 0 or 1 */
+} ai3_conv2d_params;
+
+typedef struct ai3_plan ai3_plan;
+
+/* ------------------------------------------------------------------ host-only queries */
+
+/* Library version (AI3_VERSION). */
+int ai3_version(void);
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char* ai3_last_error(void);
+
+/* Name <-> enum.  ai3_algo_name returns a static string ("?" for invalid values).
+ * ai3_algo_from_name: AI3_ERR_UNKNOWN_ALGORITHM if `name` is not one of the names above. */
+const char* ai3_algo_name(ai3_algo algo);
+ai3_status ai3_algo_from_name(const char* name, ai3_algo* out);
+
+/* out_shape = {N, K, P, Q} for in_shape = {N, C, H, W}. */
+ai3_status ai3_conv2d_output_shape(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                   int64_t out_shape[4]);
+
+/* AI3_OK if `algo` can run this problem, else AI3_ERR_UNSUPPORTED / AI3_ERR_SHAPE with
+ * a message naming the violated constraint.  GUESS is always supported
+ * for a valid shape (it resolves to a supported algorithm). */
+ai3_status ai3_conv2d_supported(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                ai3_dtype dtype, ai3_math math, ai3_algo algo);
+
+/* The algorithm GUESS resolves to: a deterministic rule over the problem
+ * (PAPER.md:190/:200 use cuDNN's heuristic; ours is DESIGN.md "guess rule").
+ * Never returns an algorithm ai3_conv2d_supported rejects. */
+ai3_status ai3_conv2d_guess(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                            ai3_dtype dtype, ai3_math math, ai3_algo* out);
+
+/* Device workspace bytes the stateless ai3_conv2d needs for this problem
+ * (includes prepared weights).  in_layout/out_layout are ai3_layout values. */
+ai3_status ai3_conv2d_workspace_size(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                     ai3_dtype dtype, ai3_math math, ai3_algo algo,
+                                     int32_t in_layout, int32_t out_layout, size_t* bytes);
+
+/* ------------------------------------------------------------------ stateless compute */
+
+/* The north_star call conv2d(input, weight, bias, stride, padding, dilation, groups,
+ * algorithm).  x: (N,C,H,W) device tensor (NCHW or NHWC); w: (K,C/G,R,S) KCRS device
+ * tensor of x's dtype; bias: K device elements of x's dtype or NULL; y: caller-allocated
+ * (N,K,P,Q) device tensor of x's dtype in y->layout.  Prepares weights into `workspace`
+ * on every call (use a plan to do that once).  workspace: device, 256-byte aligned,
+ * >= ai3_conv2d_workspace_size bytes.  Enqueued on `stream`. */
+ai3_status ai3_conv2d(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias,
+                      const int32_t stride[2], const int32_t padding[2], const int32_t dilation[2],
+                      int32_t groups, ai3_algo algo, ai3_math math, ai3_tensor4d* y,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ plans (swap-time prep) */
+
+/* Bytes of device memory the plan keeps its prepared weights in (packed / cast /
+ * Winograd-transformed weights and an fp32 bias).  GUESS is resolved first. */
+ai3_status ai3_conv2d_plan_weight_bytes(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                        ai3_dtype dtype, ai3_math math, ai3_algo algo,
+                                        size_t* bytes);
+
+/* Create a plan for inputs of exactly in_shape in in_layout, producing out_layout.
+ * w (KCRS) and bias (K or NULL) are device pointers of `dtype`, read once: the weight
+ * preparation kernels are enqueued on `stream` and write `weight_buf` (device,
+ * 256-byte aligned, >= plan_weight_bytes), which the caller keeps alive until
+ * ai3_conv2d_plan_destroy.  `w`/`bias` may be freed once `stream` has passed
+ * the preparation.  *out receives the plan (host memory owned by the library). */
+ai3_status ai3_conv2d_plan_create(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                  ai3_dtype dtype, ai3_math math, ai3_algo algo,
+                                  int32_t in_layout, int32_t out_layout,
+                                  const void* w, const void* bias,
+                                  void* weight_buf, size_t weight_bytes, void* stream,
+                                  ai3_plan** out);
+
+/* The concrete algorithm the plan runs (GUESS resolved). */
+ai3_algo ai3_conv2d_plan_algo(const ai3_plan* plan);
+
+/* Device workspace bytes ai3_conv2d_plan_execute needs (may be 0). */
+size_t ai3_conv2d_plan_workspace_size(const ai3_plan* plan);
+
+/* Number of kernels one ai3_conv2d_plan_execute enqueues. */
+int ai3_conv2d_plan_num_launches(const ai3_plan* plan);
+
+/* y = conv(x) with the plan's weights.  x, y: device pointers, contiguous in the plan's
+ * in/out layout and dtype.  workspace: device, 256-byte aligned (NULL if size 0). */
+ai3_status ai3_conv2d_plan_execute(ai3_plan* plan, const void* x, void* y,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same, from and to HOST memory: copies x_host -> x_dev (H2D), executes, copies
+ * y_dev -> y_host (D2H), all enqueued on `stream`.  x_dev / y_dev are caller-owned
+ * device staging buffers of the input / output size; host buffers should be pinned
+ * for asynchronous copies.  The caller synchronises `stream` before reading y_host. */
+ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void* y_host,
+                                        void* x_dev, void* y_dev,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Free the plan's host-side state (never the caller's device buffers). NULL is a no-op. */
+void ai3_conv2d_plan_destroy(ai3_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AI3_H */

@@ -1,0 +1,692 @@
+// api.cu -- the C ABI of libai3 (include/ai3.h): validation, output shape, the
+// `guess` rule, workspace sizing, plans and per-algorithm dispatch.
+//
+// Host logic only; every byte of the convolution is produced by the kernels in
+// direct.cu / prep.cu / transforms.cu / tc_engine.cu.  There is no CPU fallback:
+// a problem no kernel supports returns AI3_ERR_UNSUPPORTED.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <cstdarg>
+#include "internal.h"
+
+using namespace ai3;
+
+// ---------------------------------------------------------------- errors
+namespace {
+thread_local std::string g_err;
+
+ai3_status fail(ai3_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+ai3_status ok() { return AI3_OK; }
+
+ai3_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(AI3_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr size_t ALIGN = 256;
+size_t align_up(size_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct NameEntry { const char* name; ai3_algo algo; };
+const NameEntry kNames[] = {
+    {"guess", AI3_ALGO_GUESS}, {"default", AI3_ALGO_GUESS}, {"auto", AI3_ALGO_GUESS},
+    {"direct", AI3_ALGO_DIRECT}, {"gemm", AI3_ALGO_GEMM}, {"im2col", AI3_ALGO_GEMM},
+    {"implicit_gemm", AI3_ALGO_IMPLICIT_GEMM}, {"winograd", AI3_ALGO_WINOGRAD},
+    {"implicit_precomp_gemm", AI3_ALGO_IMPLICIT_PRECOMP_GEMM}, {"smm", AI3_ALGO_SMM},
+    {"kn2row", AI3_ALGO_KN2ROW}, {"custom", AI3_ALGO_CUSTOM},
+};
+
+// ---------------------------------------------------------------- problem validation
+ai3_status make_problem(const ai3_conv2d_params* p, const int64_t in[4], ai3_dtype dt, ai3_math math,
+                        ConvProblem* out) {
+    if (!p || !in || !out) return fail(AI3_ERR_INVALID_ARGUMENT, "null params / shape pointer");
+    if (in[0] < 1 || in[1] < 1 || in[2] < 1 || in[3] < 1)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "input extents must be >= 1, got (%lld,%lld,%lld,%lld)",
+                    (long long)in[0], (long long)in[1], (long long)in[2], (long long)in[3]);
+    if (p->out_channels < 1 || p->kernel[0] < 1 || p->kernel[1] < 1)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "out_channels and kernel extents must be >= 1");
+    if (p->stride[0] < 1 || p->stride[1] < 1)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "stride must be >= 1, got (%d,%d)", p->stride[0], p->stride[1]);
+    if (p->dilation[0] < 1 || p->dilation[1] < 1)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "dilation must be >= 1, got (%d,%d)", p->dilation[0], p->dilation[1]);
+    if (p->padding[0] < 0 || p->padding[1] < 0)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "padding must be >= 0, got (%d,%d)", p->padding[0], p->padding[1]);
+    if (p->groups < 1) return fail(AI3_ERR_INVALID_ARGUMENT, "groups must be >= 1, got %d", p->groups);
+    if (dt != AI3_F32 && dt != AI3_BF16) return fail(AI3_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
+    if (math != AI3_MATH_STRICT && math != AI3_MATH_TF32)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "unknown math mode %d", (int)math);
+    if (in[1] % p->groups != 0 || p->out_channels % p->groups != 0)
+        return fail(AI3_ERR_SHAPE, "groups=%d must divide in_channels=%lld and out_channels=%lld", p->groups,
+                    (long long)in[1], (long long)p->out_channels);
+    ConvProblem& c = *out;
+    c.N = in[0]; c.C = in[1]; c.H = in[2]; c.W = in[3];
+    c.K = p->out_channels; c.R = p->kernel[0]; c.S = p->kernel[1];
+    c.sh = p->stride[0]; c.sw = p->stride[1]; c.ph = p->padding[0]; c.pw = p->padding[1];
+    c.dh = p->dilation[0]; c.dw = p->dilation[1]; c.G = p->groups;
+    c.has_bias = p->has_bias != 0;
+    c.dtype = dt; c.math = math;
+    c.in_layout = AI3_NCHW; c.out_layout = AI3_NCHW;
+    // SPEC.md:120 floor formula; "kernel larger than padded input"
+    const int64_t eh = (int64_t)c.dh * (c.R - 1) + 1, ew = (int64_t)c.dw * (c.S - 1) + 1;
+    if (eh > c.H + 2 * c.ph || ew > c.W + 2 * c.pw)
+        return fail(AI3_ERR_SHAPE,
+                    "effective kernel %lldx%lld (kernel %lldx%lld, dilation %dx%d) is larger than the padded input "
+                    "%lldx%lld",
+                    (long long)eh, (long long)ew, (long long)c.R, (long long)c.S, c.dh, c.dw,
+                    (long long)(c.H + 2 * c.ph), (long long)(c.W + 2 * c.pw));
+    c.P = (c.H + 2 * c.ph - eh) / c.sh + 1;
+    c.Q = (c.W + 2 * c.pw - ew) / c.sw + 1;
+    return ok();
+}
+
+ComputeMode compute_mode(const ConvProblem& c) {
+    if (c.dtype == AI3_BF16) return CM_BF16;
+    return c.math == AI3_MATH_TF32 ? CM_TF32 : CM_3XTF32;
+}
+
+// Channels padded to a 32-byte multiple (TMA strides are 16-byte multiples; the
+// smallest swizzled K-block row is 32 bytes).
+int64_t padded_channels(int64_t C, int elem) {
+    const int64_t m = 32 / elem;
+    return C % m == 0 ? C : round_up(C, m);
+}
+
+// K-block row width for the implicit GEMM: the widest swizzle that divides a pixel's channels.
+int implicit_row_bytes(int64_t Cpad, int elem) {
+    const int64_t b = Cpad * elem;
+    return b % 128 == 0 ? 128 : (b % 64 == 0 ? 64 : 32);
+}
+
+int tiled_row_bytes(int64_t kred_bytes) { return kred_bytes >= 128 ? 128 : (kred_bytes >= 64 ? 64 : 32); }
+
+ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
+    switch (algo) {
+        case AI3_ALGO_GUESS:
+        case AI3_ALGO_DIRECT:
+            return ok();
+        case AI3_ALGO_IMPLICIT_GEMM: {
+            if (c.G != 1)
+                return fail(AI3_ERR_UNSUPPORTED, "implicit_gemm requires groups == 1 (got %d); use direct", c.G);
+            // TMA im2col bounding-box corners are signed 8-bit per spatial dim, tap offsets unsigned 8-bit
+            const int64_t up_h = c.ph - (c.R - 1) * c.dh, up_w = c.pw - (c.S - 1) * c.dw;
+            if (c.ph > 128 || c.pw > 128 || up_h < -128 || up_h > 127 || up_w < -128 || up_w > 127)
+                return fail(AI3_ERR_UNSUPPORTED,
+                            "implicit_gemm: padding / dilated kernel extent outside the TMA im2col window range");
+            if ((c.R - 1) * c.dh > 255 || (c.S - 1) * c.dw > 255)
+                return fail(AI3_ERR_UNSUPPORTED, "implicit_gemm: dilated kernel extent > 256");
+            if (c.N * c.P * c.Q >= (1LL << 31))
+                return fail(AI3_ERR_UNSUPPORTED, "implicit_gemm: N*P*Q >= 2^31 output pixels");
+            return ok();
+        }
+        case AI3_ALGO_GEMM:
+            if (c.G != 1) return fail(AI3_ERR_UNSUPPORTED, "gemm requires groups == 1 (got %d); use direct", c.G);
+            if (c.N * c.P * c.Q >= (1LL << 31))
+                return fail(AI3_ERR_UNSUPPORTED, "gemm: N*P*Q >= 2^31 output pixels");
+            return ok();
+        case AI3_ALGO_WINOGRAD:
+            if (c.R != 3 || c.S != 3)
+                return fail(AI3_ERR_UNSUPPORTED, "winograd F(2x2,3x3) requires a 3x3 kernel (got %lldx%lld)",
+                            (long long)c.R, (long long)c.S);
+            if (c.sh != 1 || c.sw != 1)
+                return fail(AI3_ERR_UNSUPPORTED, "winograd requires stride 1 (got %dx%d)", c.sh, c.sw);
+            if (c.dh != 1 || c.dw != 1)
+                return fail(AI3_ERR_UNSUPPORTED, "winograd requires dilation 1 (got %dx%d)", c.dh, c.dw);
+            if (c.G != 1) return fail(AI3_ERR_UNSUPPORTED, "winograd requires groups == 1 (got %d)", c.G);
+            if (c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2) >= (1LL << 31))
+                return fail(AI3_ERR_UNSUPPORTED, "winograd: tile count >= 2^31");
+            return ok();
+        case AI3_ALGO_IMPLICIT_PRECOMP_GEMM:
+        case AI3_ALGO_SMM:
+        case AI3_ALGO_KN2ROW:
+        case AI3_ALGO_CUSTOM:
+            return fail(AI3_ERR_UNSUPPORTED, "algorithm '%s' is reserved and not built yet", ai3_algo_name(algo));
+    }
+    return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
+}
+
+// The `guess` rule (PAPER.md:190/:200 defer to cuDNN's heuristic).
+// First matching clause wins; deterministic in (shape, params, dtype, math).
+ai3_algo guess_rule(const ConvProblem& c) {
+    if (c.G != 1) return AI3_ALGO_DIRECT;                       // only direct supports groups
+    const double macs = (double)c.N * c.K * c.C * c.R * c.S * c.P * c.Q;
+    if (macs < 16.0e6) return AI3_ALGO_DIRECT;                  // launch-bound: one kernel, no prep pass
+    if (check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
+    g_err.clear();
+    return AI3_ALGO_GEMM;
+}
+
+ai3_status resolve_algo(const ConvProblem& c, ai3_algo algo, ai3_algo* out) {
+    if ((int)algo < 0 || (int)algo > (int)AI3_ALGO_CUSTOM)
+        return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
+    ai3_status s = check_supported(c, algo);
+    if (s != AI3_OK) return s;
+    *out = algo == AI3_ALGO_GUESS ? guess_rule(c) : algo;
+    return ok();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- the plan
+struct ai3_plan {
+    ConvProblem pb{};
+    ai3_algo algo = AI3_ALGO_DIRECT;
+    ComputeMode cm = CM_BF16;
+    int elem = 2, splits = 1;
+    int64_t Cpad = 0;
+    bool need_prep = false;
+    ComputeMode prep_cm = CM_BF16;
+    // weight buffer regions (byte offsets into wbuf)
+    char* wbuf = nullptr;
+    size_t w_off = 0, wlo_off = 0, bias_off = 0, wbytes = 0;
+    bool bias_present = false;
+    int64_t Kgp = 0;  // direct: padded K per group
+    // workspace regions (byte offsets)
+    size_t ws_x = 0, ws_xlo = 0, ws_A = 0, ws_Alo = 0, ws_V = 0, ws_Vlo = 0, ws_M = 0, ws_bytes = 0;
+    // engine
+    TcPlan tc{};
+    CUtensorMap tb0{}, tb1{};
+    std::mutex mu;
+    const void* cached_a_src = nullptr;
+    CUtensorMap ta0{}, ta1{};
+    int launches = 1;
+};
+
+namespace {
+
+CUtensorMapDataType map_dtype(ComputeMode cm) {
+    return cm == CM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+}
+CUtensorMapSwizzle map_swizzle(int row_bytes) {
+    return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// Fill sizes / offsets of a plan (no device work).  algo must be resolved.
+ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
+    pl.pb = c;
+    pl.algo = algo;
+    pl.cm = compute_mode(c);
+    pl.elem = cm_elem_bytes(pl.cm);
+    pl.splits = cm_splits(pl.cm);
+    pl.bias_present = c.has_bias;
+    const size_t e = (size_t)pl.elem;
+    size_t off = 0;
+    if (algo == AI3_ALGO_DIRECT) {
+        const int64_t Kg = c.K / c.G, Cg = c.C / c.G;
+        pl.Kgp = round_up(Kg, 32);
+        pl.w_off = 0;
+        off = align_up((size_t)c.G * Cg * c.R * c.S * pl.Kgp * 4);
+        pl.bias_off = off;
+        if (c.has_bias) off = align_up(off + (size_t)c.K * 4);
+        pl.wbytes = off;
+        pl.ws_bytes = 0;
+        pl.launches = 1;
+        return ok();
+    }
+    pl.Cpad = padded_channels(c.C, pl.elem);
+    const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad : (size_t)c.K * c.R * c.S * pl.Cpad;
+    pl.w_off = 0;
+    off = align_up(wcount * e);
+    pl.wlo_off = off;
+    if (pl.splits == 2) off = align_up(off + wcount * e);
+    pl.bias_off = off;
+    if (c.has_bias) off = align_up(off + (size_t)c.K * 4);
+    pl.wbytes = off;
+
+    // input preparation pass
+    const bool nhwc_exact = c.in_layout == AI3_NHWC && pl.Cpad == c.C;
+    if (algo == AI3_ALGO_WINOGRAD) {
+        pl.need_prep = !nhwc_exact;  // the input transform reads bf16 / raw fp32 and rounds itself
+        pl.prep_cm = pl.cm == CM_BF16 ? CM_BF16 : CM_F32_RAW;
+    } else {
+        pl.need_prep = pl.cm != CM_BF16 || !nhwc_exact;  // fp32 operands must be rounded / split
+        pl.prep_cm = pl.cm;
+    }
+    const size_t xcount = (size_t)c.N * c.H * c.W * pl.Cpad;
+    size_t ws = 0;
+    if (pl.need_prep) {
+        pl.ws_x = ws;
+        ws = align_up(ws + xcount * e);
+        pl.ws_xlo = ws;
+        if (pl.prep_cm == CM_3XTF32) ws = align_up(ws + xcount * e);
+    }
+    const int64_t M = c.N * c.P * c.Q;
+    TcArgs& a = pl.tc.args;
+    std::memset(&a, 0, sizeof a);
+    a.cm = pl.cm;
+    a.Ncols = (int)c.K;
+    a.batch = 1;
+    a.out_bf16 = c.dtype == AI3_BF16;
+    a.out_nchw = c.out_layout == AI3_NCHW;
+    a.epi_PQ = (int)(c.P * c.Q);
+    if (algo == AI3_ALGO_IMPLICIT_GEMM) {
+        a.a_mode = TC_A_IM2COL;
+        a.M = (int)M;
+        a.row_bytes = implicit_row_bytes(pl.Cpad, pl.elem);
+        a.c_chunks = (int)(pl.Cpad * pl.elem / a.row_bytes);
+        a.num_kb = (int)(c.R * c.S * a.c_chunks);
+        a.Q = (int)c.Q; a.PQ = (int)(c.P * c.Q);
+        a.sh = c.sh; a.sw = c.sw; a.ph = c.ph; a.pw = c.pw; a.dh = c.dh; a.dw = c.dw; a.S = (int)c.S;
+        pl.launches = 1 + (pl.need_prep ? 1 : 0);
+    } else if (algo == AI3_ALGO_GEMM) {
+        const int64_t kred = c.R * c.S * pl.Cpad;
+        pl.ws_A = ws;
+        ws = align_up(ws + (size_t)M * kred * e);
+        pl.ws_Alo = ws;
+        if (pl.splits == 2) ws = align_up(ws + (size_t)M * kred * e);
+        a.a_mode = TC_A_TILED2D;
+        a.M = (int)M;
+        a.row_bytes = tiled_row_bytes(kred * pl.elem);
+        a.num_kb = (int)((kred * pl.elem + a.row_bytes - 1) / a.row_bytes);
+        pl.launches = (pl.need_prep ? 1 : 0) + pl.splits + 1;
+    } else {  // WINOGRAD
+        const int64_t T = c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2);
+        pl.ws_V = ws;
+        ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
+        pl.ws_Vlo = ws;
+        if (pl.splits == 2) ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
+        pl.ws_M = ws;
+        ws = align_up(ws + (size_t)16 * T * c.K * 4);
+        a.a_mode = TC_A_TILED3D;
+        a.M = (int)T;
+        a.batch = 16;
+        a.row_bytes = tiled_row_bytes(pl.Cpad * pl.elem);
+        a.num_kb = (int)((pl.Cpad * pl.elem + a.row_bytes - 1) / a.row_bytes);
+        a.out_bf16 = 0;        // M is fp32
+        a.epi_PQ = (int)T;     // [16][K][T] when the final output is NCHW
+        a.out_bstride = (long long)T * c.K;
+        pl.launches = (pl.need_prep ? 1 : 0) + 3;
+    }
+    pl.ws_bytes = ws;
+    tc_configure(pl.tc, device_num_sms());
+    return ok();
+}
+
+// Encode the weight-side (B) tensor maps once per plan.
+ai3_status encode_b_maps(ai3_plan& pl) {
+    const ConvProblem& c = pl.pb;
+    const TcArgs& a = pl.tc.args;
+    const CUtensorMapDataType dt = map_dtype(pl.cm);
+    const CUtensorMapSwizzle sw = map_swizzle(a.row_bytes);
+    const uint32_t kel = (uint32_t)(a.row_bytes / pl.elem);
+    const char* w = pl.wbuf + pl.w_off;
+    const char* wlo = pl.wbuf + pl.wlo_off;
+    bool okb;
+    if (pl.algo == AI3_ALGO_WINOGRAD) {
+        const uint64_t dims[3] = {(uint64_t)pl.Cpad, (uint64_t)c.K, 16};
+        const uint64_t str[2] = {(uint64_t)pl.Cpad * pl.elem, (uint64_t)c.K * pl.Cpad * pl.elem};
+        const uint32_t box[3] = {kel, (uint32_t)a.block_n, 1};
+        okb = encode_tiled(&pl.tb0, dt, 3, w, dims, str, box, sw);
+        if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 3, wlo, dims, str, box, sw);
+    } else {
+        const uint64_t kred = (uint64_t)(c.R * c.S * pl.Cpad);
+        const uint64_t dims[2] = {kred, (uint64_t)c.K};
+        const uint64_t str[1] = {kred * pl.elem};
+        const uint32_t box[2] = {kel, (uint32_t)a.block_n};
+        okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box, sw);
+        if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 2, wlo, dims, str, box, sw);
+    }
+    if (!okb) return fail(AI3_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weight operand");
+    if (pl.splits != 2) pl.tb1 = pl.tb0;
+    return ok();
+}
+
+// Encode (or reuse) the activation-side (A) tensor maps for source `src` (and src_lo).
+ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
+    if (pl.cached_a_src == src) return ok();
+    const ConvProblem& c = pl.pb;
+    const TcArgs& a = pl.tc.args;
+    const CUtensorMapDataType dt = map_dtype(pl.cm);
+    const CUtensorMapSwizzle sw = map_swizzle(a.row_bytes);
+    const uint32_t kel = (uint32_t)(a.row_bytes / pl.elem);
+    const uint64_t e = (uint64_t)pl.elem;
+    bool oka = true;
+    if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
+        const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
+        const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
+        const int lower[2] = {-c.pw, -c.ph};
+        const int upper[2] = {(int)(c.pw - (c.S - 1) * c.dw), (int)(c.ph - (c.R - 1) * c.dh)};
+        const uint32_t es[4] = {1, (uint32_t)c.sw, (uint32_t)c.sh, 1};
+        oka = encode_im2col(&pl.ta0, dt, src, dims, str, lower, upper, kel, 128, es, sw);
+        if (oka && pl.splits == 2) oka = encode_im2col(&pl.ta1, dt, src_lo, dims, str, lower, upper, kel, 128, es, sw);
+    } else if (pl.algo == AI3_ALGO_GEMM) {
+        const uint64_t kred = (uint64_t)(c.R * c.S * pl.Cpad);
+        const uint64_t dims[2] = {kred, (uint64_t)a.M};
+        const uint64_t str[1] = {kred * e};
+        const uint32_t box[2] = {kel, 128};
+        oka = encode_tiled(&pl.ta0, dt, 2, src, dims, str, box, sw);
+        if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 2, src_lo, dims, str, box, sw);
+    } else {
+        const uint64_t dims[3] = {(uint64_t)pl.Cpad, (uint64_t)a.M, 16};
+        const uint64_t str[2] = {pl.Cpad * e, (uint64_t)a.M * pl.Cpad * e};
+        const uint32_t box[3] = {kel, 128, 1};
+        oka = encode_tiled(&pl.ta0, dt, 3, src, dims, str, box, sw);
+        if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 3, src_lo, dims, str, box, sw);
+    }
+    if (!oka) {
+        pl.cached_a_src = nullptr;
+        return fail(AI3_ERR_CUDA, "tensor-map encoding failed for the activation operand (%s)",
+                    ai3_algo_name(pl.algo));
+    }
+    if (pl.splits != 2) pl.ta1 = pl.ta0;
+    pl.cached_a_src = src;
+    return ok();
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaStream_t st) {
+    const ConvProblem& c = pl.pb;
+    cudaError_t e = cudaSuccess;
+    char* wb = pl.wbuf;
+    if (pl.algo == AI3_ALGO_DIRECT) {
+        e = launch_direct_weights(w, c.dtype, c.K, c.C / c.G, c.R, c.S, c.G, pl.Kgp,
+                                  reinterpret_cast<float*>(wb + pl.w_off), st);
+    } else if (pl.algo == AI3_ALGO_WINOGRAD) {
+        e = launch_winograd_filter(w, c.dtype, c.K, c.C, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
+    } else {
+        e = launch_pack_weights(w, c.dtype, c.K, c.C, c.R, c.S, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "weight preparation launch");
+    if (pl.bias_present) {
+        e = launch_bias_f32(bias, c.dtype, c.K, reinterpret_cast<float*>(wb + pl.bias_off), st);
+        if (e != cudaSuccess) return cuda_fail(e, "bias preparation launch");
+    }
+    return ok();
+}
+
+ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const ConvProblem& c = pl.pb;
+    if (!x || !y) return fail(AI3_ERR_INVALID_ARGUMENT, "null x or y");
+    if (ws_bytes < pl.ws_bytes || (pl.ws_bytes > 0 && (!ws || !aligned(ws, ALIGN))))
+        return fail(AI3_ERR_WORKSPACE, "workspace of %zu bytes (256-byte aligned) required, got %zu", pl.ws_bytes,
+                    ws_bytes);
+    const float* bias = pl.bias_present ? reinterpret_cast<const float*>(pl.wbuf + pl.bias_off) : nullptr;
+    char* w = reinterpret_cast<char*>(ws);
+    cudaError_t e = cudaSuccess;
+    if (pl.algo == AI3_ALGO_DIRECT) {
+        DirectArgs d{};
+        d.x = x; d.w = reinterpret_cast<const float*>(pl.wbuf + pl.w_off); d.bias = bias; d.y = y;
+        d.N = c.N; d.C = c.C; d.H = c.H; d.W = c.W; d.K = c.K; d.P = c.P; d.Q = c.Q;
+        d.R = (int)c.R; d.S = (int)c.S; d.sh = c.sh; d.sw = c.sw; d.ph = c.ph; d.pw = c.pw; d.dh = c.dh; d.dw = c.dw;
+        d.G = c.G; d.Cg = (int)(c.C / c.G); d.Kg = (int)(c.K / c.G); d.Kgp = (int)pl.Kgp;
+        d.in_nhwc = c.in_layout == AI3_NHWC; d.out_nhwc = c.out_layout == AI3_NHWC; d.bf16 = c.dtype == AI3_BF16;
+        e = launch_direct(d, st);
+        if (e != cudaSuccess) return cuda_fail(e, "direct kernel launch");
+        return ok();
+    }
+    // 1. input preparation (layout / channel pad / operand precision)
+    const void* xs = x;
+    const void* xs_lo = nullptr;
+    if (pl.need_prep) {
+        e = launch_prep_input(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, pl.Cpad, pl.prep_cm, w + pl.ws_x,
+                              w + pl.ws_xlo, st);
+        if (e != cudaSuccess) return cuda_fail(e, "input preparation launch");
+        xs = w + pl.ws_x;
+        xs_lo = w + pl.ws_xlo;
+    } else if (!aligned(x, 16)) {
+        return fail(AI3_ERR_INVALID_ARGUMENT, "x must be 16-byte aligned");
+    }
+    std::lock_guard<std::mutex> lock(pl.mu);
+    TcPlan tp = pl.tc;
+    tp.args.bias = bias;
+    ai3_status s;
+    if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
+        if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
+        tp.args.out = y;
+    } else if (pl.algo == AI3_ALGO_GEMM) {
+        e = launch_im2col(xs, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph, c.pw, c.dh,
+                          c.dw, pl.elem, w + pl.ws_A, st);
+        if (e == cudaSuccess && pl.splits == 2)
+            e = launch_im2col(xs_lo, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph, c.pw,
+                              c.dh, c.dw, pl.elem, w + pl.ws_Alo, st);
+        if (e != cudaSuccess) return cuda_fail(e, "im2col launch");
+        if ((s = encode_a_maps(pl, w + pl.ws_A, w + pl.ws_Alo)) != AI3_OK) return s;
+        tp.args.out = y;
+    } else {
+        e = launch_winograd_input(xs, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, c.ph, c.pw, pl.cm, nullptr, w + pl.ws_V,
+                                  w + pl.ws_Vlo, st);
+        if (e != cudaSuccess) return cuda_fail(e, "winograd input transform launch");
+        if ((s = encode_a_maps(pl, w + pl.ws_V, w + pl.ws_Vlo)) != AI3_OK) return s;
+        tp.args.out = w + pl.ws_M;
+        tp.args.bias = nullptr;
+    }
+    e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
+    if (pl.algo == AI3_ALGO_WINOGRAD) {
+        e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,
+                                   c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, st);
+        if (e != cudaSuccess) return cuda_fail(e, "winograd output transform launch");
+    }
+    return ok();
+}
+
+ai3_status check_tensor(const ai3_tensor4d* t, const char* what) {
+    if (!t) return fail(AI3_ERR_INVALID_ARGUMENT, "%s descriptor is null", what);
+    if (!t->data) return fail(AI3_ERR_INVALID_ARGUMENT, "%s data pointer is null", what);
+    if (t->dtype != AI3_F32 && t->dtype != AI3_BF16) return fail(AI3_ERR_INVALID_ARGUMENT, "%s: unknown dtype", what);
+    if (t->layout != AI3_NCHW && t->layout != AI3_NHWC) return fail(AI3_ERR_INVALID_ARGUMENT, "%s: unknown layout", what);
+    return ok();
+}
+
+size_t act_bytes(const ConvProblem& c, bool output) {
+    const size_t e = c.dtype == AI3_BF16 ? 2 : 4;
+    return output ? (size_t)(c.N * c.K * c.P * c.Q) * e : (size_t)(c.N * c.C * c.H * c.W) * e;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int ai3_version(void) { return AI3_VERSION; }
+
+const char* ai3_last_error(void) { return g_err.c_str(); }
+
+const char* ai3_algo_name(ai3_algo algo) {
+    switch (algo) {
+        case AI3_ALGO_GUESS: return "guess";
+        case AI3_ALGO_DIRECT: return "direct";
+        case AI3_ALGO_GEMM: return "gemm";
+        case AI3_ALGO_IMPLICIT_GEMM: return "implicit_gemm";
+        case AI3_ALGO_WINOGRAD: return "winograd";
+        case AI3_ALGO_IMPLICIT_PRECOMP_GEMM: return "implicit_precomp_gemm";
+        case AI3_ALGO_SMM: return "smm";
+        case AI3_ALGO_KN2ROW: return "kn2row";
+        case AI3_ALGO_CUSTOM: return "custom";
+    }
+    return "?";
+}
+
+ai3_status ai3_algo_from_name(const char* name, ai3_algo* out) {
+    if (!name || !out) return fail(AI3_ERR_INVALID_ARGUMENT, "null name / out");
+    for (const NameEntry& e : kNames)
+        if (std::strcmp(e.name, name) == 0) { *out = e.algo; return ok(); }
+    return fail(AI3_ERR_UNKNOWN_ALGORITHM,
+                "unknown algorithm '%s' (known: guess, default, auto, direct, gemm, im2col, implicit_gemm, winograd)",
+                name);
+}
+
+ai3_status ai3_conv2d_output_shape(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                   int64_t out_shape[4]) {
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, AI3_F32, AI3_MATH_STRICT, &c);
+    if (s != AI3_OK) return s;
+    if (!out_shape) return fail(AI3_ERR_INVALID_ARGUMENT, "null out_shape");
+    out_shape[0] = c.N; out_shape[1] = c.K; out_shape[2] = c.P; out_shape[3] = c.Q;
+    return ok();
+}
+
+ai3_status ai3_conv2d_supported(const ai3_conv2d_params* params, const int64_t in_shape[4], ai3_dtype dtype,
+                                ai3_math math, ai3_algo algo) {
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, dtype, math, &c);
+    if (s != AI3_OK) return s;
+    ai3_algo r = AI3_ALGO_DIRECT;
+    return resolve_algo(c, algo, &r);
+}
+
+ai3_status ai3_conv2d_guess(const ai3_conv2d_params* params, const int64_t in_shape[4], ai3_dtype dtype,
+                            ai3_math math, ai3_algo* out) {
+    if (!out) return fail(AI3_ERR_INVALID_ARGUMENT, "null out");
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, dtype, math, &c);
+    if (s != AI3_OK) return s;
+    return resolve_algo(c, AI3_ALGO_GUESS, out);
+}
+
+ai3_status ai3_conv2d_plan_weight_bytes(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                        ai3_dtype dtype, ai3_math math, ai3_algo algo, size_t* bytes) {
+    if (!bytes) return fail(AI3_ERR_INVALID_ARGUMENT, "null bytes");
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, dtype, math, &c);
+    if (s != AI3_OK) return s;
+    ai3_algo r = AI3_ALGO_DIRECT;
+    if ((s = resolve_algo(c, algo, &r)) != AI3_OK) return s;
+    ai3_plan* pl = new (std::nothrow) ai3_plan();
+    if (!pl) return fail(AI3_ERR_INVALID_ARGUMENT, "out of host memory");
+    s = layout_plan(*pl, c, r);
+    if (s == AI3_OK) *bytes = pl->wbytes;
+    delete pl;
+    return s;
+}
+
+ai3_status ai3_conv2d_workspace_size(const ai3_conv2d_params* params, const int64_t in_shape[4], ai3_dtype dtype,
+                                     ai3_math math, ai3_algo algo, int32_t in_layout, int32_t out_layout,
+                                     size_t* bytes) {
+    if (!bytes) return fail(AI3_ERR_INVALID_ARGUMENT, "null bytes");
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, dtype, math, &c);
+    if (s != AI3_OK) return s;
+    if ((in_layout != AI3_NCHW && in_layout != AI3_NHWC) || (out_layout != AI3_NCHW && out_layout != AI3_NHWC))
+        return fail(AI3_ERR_INVALID_ARGUMENT, "unknown layout");
+    c.in_layout = in_layout;
+    c.out_layout = out_layout;
+    ai3_algo r = AI3_ALGO_DIRECT;
+    if ((s = resolve_algo(c, algo, &r)) != AI3_OK) return s;
+    ai3_plan* pl = new (std::nothrow) ai3_plan();
+    if (!pl) return fail(AI3_ERR_INVALID_ARGUMENT, "out of host memory");
+    s = layout_plan(*pl, c, r);
+    if (s == AI3_OK) *bytes = pl->wbytes + pl->ws_bytes;
+    delete pl;
+    return s;
+}
+
+ai3_status ai3_conv2d_plan_create(const ai3_conv2d_params* params, const int64_t in_shape[4], ai3_dtype dtype,
+                                  ai3_math math, ai3_algo algo, int32_t in_layout, int32_t out_layout, const void* w,
+                                  const void* bias, void* weight_buf, size_t weight_bytes, void* stream,
+                                  ai3_plan** out) {
+    if (!out) return fail(AI3_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    ConvProblem c{};
+    ai3_status s = make_problem(params, in_shape, dtype, math, &c);
+    if (s != AI3_OK) return s;
+    if ((in_layout != AI3_NCHW && in_layout != AI3_NHWC) || (out_layout != AI3_NCHW && out_layout != AI3_NHWC))
+        return fail(AI3_ERR_INVALID_ARGUMENT, "unknown layout");
+    if (!w) return fail(AI3_ERR_INVALID_ARGUMENT, "null weight pointer");
+    if (c.has_bias && !bias) return fail(AI3_ERR_INVALID_ARGUMENT, "has_bias set but bias pointer is null");
+    c.in_layout = in_layout;
+    c.out_layout = out_layout;
+    ai3_algo r = AI3_ALGO_DIRECT;
+    if ((s = resolve_algo(c, algo, &r)) != AI3_OK) return s;
+    ai3_plan* pl = new (std::nothrow) ai3_plan();
+    if (!pl) return fail(AI3_ERR_INVALID_ARGUMENT, "out of host memory");
+    if ((s = layout_plan(*pl, c, r)) != AI3_OK) { delete pl; return s; }
+    if (!weight_buf || weight_bytes < pl->wbytes || !aligned(weight_buf, ALIGN)) {
+        const size_t need = pl->wbytes;
+        delete pl;
+        return fail(AI3_ERR_WORKSPACE, "weight buffer of %zu bytes (256-byte aligned) required, got %zu", need,
+                    weight_bytes);
+    }
+    pl->wbuf = reinterpret_cast<char*>(weight_buf);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if ((s = prepare_weights(*pl, w, bias, st)) != AI3_OK) { delete pl; return s; }
+    if (r != AI3_ALGO_DIRECT && (s = encode_b_maps(*pl)) != AI3_OK) { delete pl; return s; }
+    *out = pl;
+    return ok();
+}
+
+ai3_algo ai3_conv2d_plan_algo(const ai3_plan* plan) { return plan ? plan->algo : AI3_ALGO_GUESS; }
+
+size_t ai3_conv2d_plan_workspace_size(const ai3_plan* plan) { return plan ? plan->ws_bytes : 0; }
+
+int ai3_conv2d_plan_num_launches(const ai3_plan* plan) { return plan ? plan->launches : 0; }
+
+ai3_status ai3_conv2d_plan_execute(ai3_plan* plan, const void* x, void* y, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+    if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
+    return execute(*plan, x, y, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void* y_host, void* x_dev, void* y_dev,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+    if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
+    if (!x_host || !y_host || !x_dev || !y_dev) return fail(AI3_ERR_INVALID_ARGUMENT, "null host or staging buffer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(x_dev, x_host, act_bytes(plan->pb, false), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
+    ai3_status s = execute(*plan, x_dev, y_dev, workspace, workspace_bytes, st);
+    if (s != AI3_OK) return s;
+    e = cudaMemcpyAsync(y_host, y_dev, act_bytes(plan->pb, true), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy of y");
+    return ok();
+}
+
+void ai3_conv2d_plan_destroy(ai3_plan* plan) { delete plan; }
+
+ai3_status ai3_conv2d(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias, const int32_t stride[2],
+                      const int32_t padding[2], const int32_t dilation[2], int32_t groups, ai3_algo algo,
+                      ai3_math math, ai3_tensor4d* y, void* workspace, size_t workspace_bytes, void* stream) {
+    ai3_status s;
+    if ((s = check_tensor(x, "x")) != AI3_OK || (s = check_tensor(w, "w")) != AI3_OK ||
+        (s = check_tensor(y, "y")) != AI3_OK)
+        return s;
+    if (!stride || !padding || !dilation) return fail(AI3_ERR_INVALID_ARGUMENT, "null stride/padding/dilation");
+    if (w->dtype != x->dtype || y->dtype != x->dtype)
+        return fail(AI3_ERR_INVALID_ARGUMENT, "x, w and y must share one dtype");
+    if (w->layout != AI3_NCHW) return fail(AI3_ERR_INVALID_ARGUMENT, "weights must be KCRS (AI3_NCHW layout)");
+    if (groups < 1) return fail(AI3_ERR_INVALID_ARGUMENT, "groups must be >= 1, got %d", groups);
+    if (w->c * groups != x->c)
+        return fail(AI3_ERR_SHAPE, "weight has %lld input channels per group x %d groups, input has %lld channels",
+                    (long long)w->c, groups, (long long)x->c);
+    if (w->h > INT32_MAX || w->w > INT32_MAX) return fail(AI3_ERR_SHAPE, "kernel too large");
+    ai3_conv2d_params p{};
+    p.out_channels = w->n;
+    p.kernel[0] = (int32_t)w->h; p.kernel[1] = (int32_t)w->w;
+    p.stride[0] = stride[0]; p.stride[1] = stride[1];
+    p.padding[0] = padding[0]; p.padding[1] = padding[1];
+    p.dilation[0] = dilation[0]; p.dilation[1] = dilation[1];
+    p.groups = groups;
+    p.has_bias = bias != nullptr;
+    const int64_t in_shape[4] = {x->n, x->c, x->h, x->w};
+    int64_t os[4];
+    if ((s = ai3_conv2d_output_shape(&p, in_shape, os)) != AI3_OK) return s;
+    if (y->n != os[0] || y->c != os[1] || y->h != os[2] || y->w != os[3])
+        return fail(AI3_ERR_SHAPE, "output tensor is (%lld,%lld,%lld,%lld), expected (%lld,%lld,%lld,%lld)",
+                    (long long)y->n, (long long)y->c, (long long)y->h, (long long)y->w, (long long)os[0],
+                    (long long)os[1], (long long)os[2], (long long)os[3]);
+    ai3_plan* pl = nullptr;
+    size_t wbytes = 0;
+    if ((s = ai3_conv2d_plan_weight_bytes(&p, in_shape, (ai3_dtype)x->dtype, math, algo, &wbytes)) != AI3_OK) return s;
+    if (!workspace || workspace_bytes < wbytes)
+        return fail(AI3_ERR_WORKSPACE, "workspace too small for the prepared weights (%zu bytes needed)", wbytes);
+    if ((s = ai3_conv2d_plan_create(&p, in_shape, (ai3_dtype)x->dtype, math, algo, x->layout, y->layout, w->data,
+                                     bias, workspace, wbytes, stream, &pl)) != AI3_OK)
+        return s;
+    char* ws = reinterpret_cast<char*>(workspace) + wbytes;
+    s = ai3_conv2d_plan_execute(pl, x->data, y->data, pl->ws_bytes ? ws : nullptr, workspace_bytes - wbytes, stream);
+    ai3_conv2d_plan_destroy(pl);
+    return s;
+}
+
+}  // extern "C"

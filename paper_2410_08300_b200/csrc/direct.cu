@@ -1,0 +1,146 @@
+// direct.cu -- the `direct` algorithm (§II.B(d): "kernels are applied
+// directly to the input without transforming the data").
+//
+// CUDA-core FFMA with fp32 accumulation.  One CTA (256 threads) computes a tile of
+// 32 output channels x (8 rows x 32 columns) output pixels of one image / group.
+// Per channel chunk the CTA stages the input footprint and the 32 channels'
+// weights in shared memory (k fastest, so a thread's 8 weights are two
+// broadcast 128-bit loads); each thread then accumulates 8 channels x 4
+// pixels = 32 fp32 accumulators over (c, r, s) in that order.
+// Handles any stride / padding / dilation / groups and NCHW or NHWC, fp32 or bf16.
+#include <cuda_bf16.h>
+#include "internal.h"
+
+namespace ai3 {
+
+namespace {
+constexpr int TK = 32, TP = 8, TQ = 32, NT = 256;
+
+__device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
+    return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
+}
+}  // namespace
+
+template <int KS>
+__global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp) {
+    extern __shared__ float smem[];
+    const int R = KS ? KS : a.R;
+    const int S = KS ? KS : a.S;
+    const int tid = threadIdx.x;
+    const int qg = tid & 7, pr = (tid >> 3) & 7, kg = tid >> 6;
+    const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
+    const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
+    const int k0g = blockIdx.y * TK;
+    const int n = blockIdx.z / a.G, g = blockIdx.z % a.G;
+    const int ih0 = p0 * a.sh - a.ph, iw0 = q0 * a.sw - a.pw;
+
+    float* xs = smem;                         // [CB][FH][FWp]
+    float* ws = smem + (size_t)CB * FH * FWp;  // [CB][R][S][TK]
+
+    float acc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
+
+    const int64_t xsN = a.in_nhwc ? a.H * a.W * a.C : a.C * a.H * a.W;
+    const int64_t xsC = a.in_nhwc ? 1 : a.H * a.W;
+    const int64_t xsH = a.in_nhwc ? a.W * a.C : a.W;
+    const int64_t xsW = a.in_nhwc ? a.C : 1;
+    const int64_t xbase = (int64_t)n * xsN + (int64_t)g * a.Cg * xsC;
+
+    for (int c0 = 0; c0 < a.Cg; c0 += CB) {
+        const int cb = min(CB, a.Cg - c0);
+        // ---- stage input footprint
+        const int nx = cb * FH * FW;
+        for (int idx = tid; idx < nx; idx += NT) {
+            int cc, y, xw;
+            if (a.in_nhwc) { cc = idx % cb; const int t = idx / cb; xw = t % FW; y = t / FW; }
+            else { xw = idx % FW; const int t = idx / FW; y = t % FH; cc = t / FH; }
+            const int ih = ih0 + y, iw = iw0 + xw;
+            float v = 0.f;
+            if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
+                v = ldx(a.x, xbase + (int64_t)(c0 + cc) * xsC + (int64_t)ih * xsH + (int64_t)iw * xsW, a.bf16);
+            xs[(cc * FH + y) * FWp + xw] = v;
+        }
+        // ---- stage weights [cc][r][s][TK] (contiguous rows of the prepared layout)
+        const int nw = cb * R * S * TK;
+        for (int idx = tid; idx < nw; idx += NT) {
+            const int kk = idx % TK;
+            const int t = idx / TK;  // (cc, r, s)
+            ws[idx] = a.w[((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S + t) * a.Kgp + k0g + kk];
+        }
+        __syncthreads();
+        for (int cc = 0; cc < cb; ++cc) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                const float* xrow = xs + (cc * FH + pr * a.sh + rr * a.dh) * FWp + qg * 4 * a.sw;
+                const float* wrow = ws + ((cc * R + rr) * S) * TK + kg * 8;
+#pragma unroll
+                for (int ss = 0; ss < S; ++ss) {
+                    const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
+                    const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
+                    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                    float xv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[i] = xrow[i * a.sw + ss * a.dw];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(wv[j], xv[i], acc[j][i]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: bias once at the end, cast, store
+    const int p = p0 + pr;
+    if (p >= a.P) return;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int kk = k0g + kg * 8 + j;
+        if (kk >= a.Kg) break;
+        const int64_t k = (int64_t)g * a.Kg + kk;
+        const float bv = a.bias ? a.bias[k] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int q = q0 + qg * 4 + i;
+            if (q >= a.Q) break;
+            const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + q) * a.K + k
+                                         : (((int64_t)n * a.K + k) * a.P + p) * a.Q + q;
+            const float v = acc[j][i] + bv;
+            if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
+            else reinterpret_cast<float*>(a.y)[o] = v;
+        }
+    }
+}
+
+cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
+    const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
+    const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
+    int FWp = FW;
+    while (FWp % 4 != 1) ++FWp;  // row stride = 1 mod 4: the 4 rows of a warp hit distinct banks
+    const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
+    const int budget = 64 * 1024;
+    int CB = budget / per_c;
+    if (CB < 1) CB = 1;
+    if (CB > a.Cg) CB = a.Cg;
+    const size_t smem = (size_t)CB * per_c;
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
+    dim3 grid(tiles, (unsigned)((a.Kg + TK - 1) / TK), (unsigned)(a.N * a.G));
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp);
+    };
+    if (a.R == a.S && a.R == 3) launch(direct_conv_kernel<3>);
+    else if (a.R == a.S && a.R == 1) launch(direct_conv_kernel<1>);
+    else if (a.R == a.S && a.R == 5) launch(direct_conv_kernel<5>);
+    else if (a.R == a.S && a.R == 7) launch(direct_conv_kernel<7>);
+    else if (a.R == a.S && a.R == 11) launch(direct_conv_kernel<11>);
+    else launch(direct_conv_kernel<0>);
+    return cudaGetLastError();
+}
+
+}  // namespace ai3

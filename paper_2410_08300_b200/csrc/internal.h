@@ -1,0 +1,123 @@
+// internal.h -- shared host/device declarations of libai3 (not part of the ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda.h>
+
+#include "../../include/ai3.h"
+
+namespace ai3 {
+
+// How the tensor-core algorithms multiply.
+enum ComputeMode : int {
+    CM_BF16 = 0,   // bf16 operands, fp32 accumulate (tcgen05 kind::f16)
+    CM_TF32 = 1,   // fp32 operands rounded to tf32 (nearest), fp32 accumulate (kind::tf32)
+    CM_3XTF32 = 2, // fp32-accurate: a = a_hi + a_lo (both tf32), acc += a_lo*b_hi + a_hi*b_lo + a_hi*b_hi
+    CM_F32_RAW = 3 // (prep only) plain fp32 copy, rounding deferred to a later transform
+};
+
+inline int cm_elem_bytes(ComputeMode cm) { return cm == CM_BF16 ? 2 : 4; }
+inline int cm_splits(ComputeMode cm) { return cm == CM_3XTF32 ? 2 : 1; }
+
+struct ConvProblem {
+    int64_t N, C, H, W, K, R, S, P, Q;
+    int sh, sw, ph, pw, dh, dw, G;
+    bool has_bias;
+    ai3_dtype dtype;
+    ai3_math math;
+    int in_layout, out_layout;
+};
+
+// ---------------------------------------------------------------- prep kernels (prep.cu)
+// x (NCHW or NHWC, dtype) -> dst NHWC with Cpad channels in compute mode
+// (CM_3XTF32 also writes dst_lo).  Zero channels beyond C.
+cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H,
+                              int64_t W, int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo,
+                              cudaStream_t st);
+// KCRS weights -> [K][R][S][Cpad] in compute mode (+ lo).
+cudaError_t launch_pack_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
+// KCRS (3x3) weights -> U[16][K][Cpad] = G g G^T, in compute mode (+ lo).
+cudaError_t launch_winograd_filter(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t Cpad,
+                                   ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
+// KCRS (grouped: K x Cg x R x S) -> fp32 [G][Cg][R][S][Kgp] (k fastest, zero padded).
+cudaError_t launch_direct_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t Cg, int64_t R, int64_t S,
+                                  int G, int64_t Kgp, float* dst, cudaStream_t st);
+// bias (dtype) -> fp32
+cudaError_t launch_bias_f32(const void* b, ai3_dtype dtype, int64_t K, float* dst, cudaStream_t st);
+
+// ---------------------------------------------------------------- direct (direct.cu)
+struct DirectArgs {
+    const void* x;        // input, dtype, in_layout
+    const float* w;       // [G][Cg][R][S][Kgp]
+    const float* bias;    // fp32 [K] or null
+    void* y;              // output, dtype, out_layout
+    int64_t N, C, H, W, K, P, Q;
+    int R, S, sh, sw, ph, pw, dh, dw, G, Cg, Kg, Kgp;
+    int in_nhwc, out_nhwc, bf16;
+};
+cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- im2col / winograd transforms
+// NHWC (Cpad) -> A[M][R*S*Cpad], column order (r, s, c).
+cudaError_t launch_im2col(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P, int64_t Q,
+                          int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int elem_bytes, void* A,
+                          cudaStream_t st);
+// NHWC (Cpad) -> V[16][T][Cpad], T = N*ceil(P/2)*ceil(Q/2), rounded per compute mode (+ lo).
+cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P,
+                                  int64_t Q, int ph, int pw, ComputeMode cm, const void* x_lo, void* V, void* V_lo,
+                                  cudaStream_t st);
+// M (fp32, [16][K][T] if out NCHW else [16][T][K]) -> y (+bias), cropped to P x Q.
+cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
+                                   int64_t N, int64_t K, int64_t P, int64_t Q, cudaStream_t st);
+
+// ---------------------------------------------------------------- tcgen05 engine (tc_engine.cu)
+enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2 };
+
+struct TcArgs {
+    int a_mode;     // TcAMode
+    int cm;         // ComputeMode
+    int M;          // GEMM rows per batch
+    int Ncols;      // GEMM columns (output channels)
+    int batch;      // independent GEMMs (Winograd: 16)
+    int block_n;    // 32 / 64 / 128 / 256
+    int row_bytes;  // 32 / 64 / 128: bytes of one K-block row (swizzle width)
+    int num_kb;     // K-blocks per tile
+    int stages;
+    int m_tiles, n_tiles;
+    // im2col coordinates (a_mode == TC_A_IM2COL)
+    int Q, PQ, sh, sw, ph, pw, dh, dw, S, c_chunks;
+    // epilogue
+    int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
+    int out_bf16;
+    int epi_PQ;
+    const float* bias;  // fp32 [Ncols] or null
+    void* out;
+    long long out_bstride;  // elements between batches
+};
+
+struct TcPlan {
+    TcArgs args;
+    int smem_bytes;
+    int grid;
+    int tmem_cols;
+};
+
+// Choose tiles/stages for a GEMM of M x Ncols x Kred (Kred only for TILED modes) and fill
+// the shape fields of args (a_mode, cm, M, Ncols, batch, row_bytes, num_kb must be set).
+void tc_configure(TcPlan& p, int num_sms);
+// Encode the tensor maps and launch.  a0/a1/b0/b1 are prepared by the caller.
+cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b0,
+                      const CUtensorMap* b1, cudaStream_t st);
+
+// Driver entry points for tensor-map encoding (resolved once via cudaGetDriverEntryPoint).
+bool encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* addr, const uint64_t* dims,
+                  const uint64_t* strides_bytes /* rank-1 */, const uint32_t* box, CUtensorMapSwizzle sw);
+bool encode_im2col(CUtensorMap* m, CUtensorMapDataType dt, const void* addr, const uint64_t dims[4],
+                   const uint64_t strides_bytes[3], const int lower[2], const int upper[2], uint32_t channels,
+                   uint32_t pixels, const uint32_t estrides[4], CUtensorMapSwizzle sw);
+
+int device_num_sms();
+
+}  // namespace ai3

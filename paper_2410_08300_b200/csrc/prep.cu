@@ -1,0 +1,177 @@
+// prep.cu -- layout / precision preparation kernels.
+//
+//  * launch_prep_input: NCHW|NHWC activations -> NHWC with the channel count
+//    padded to a 32-byte multiple, in the tensor cores' operand precision
+//    (bf16 copy, tf32 round-to-nearest, or the 3xTF32 hi/lo split).
+//  * launch_pack_weights: KCRS -> [K][R][S][Cpad] (the K-major B operand of the
+//    implicit / explicit GEMM, reduction order (r, s, c)).
+//  * launch_winograd_filter: U = G g G^T per (k, c) (Lavin-Gray
+//    F(2x2,3x3) matrices, reading R10) -> [16][K][Cpad].
+//  * launch_direct_weights: KCRS -> fp32 [G][Cg][R][S][Kg padded] for the FFMA kernel.
+#include <cuda_bf16.h>
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace ai3 {
+
+__device__ __forceinline__ float load_as_f32(const void* p, int64_t i, int bf16) {
+    return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i])
+                : reinterpret_cast<const float*>(p)[i];
+}
+
+// Store v in compute-mode representation at dst[i] (and dst_lo[i] for 3xTF32).
+__device__ __forceinline__ void store_cm(void* dst, void* dst_lo, int64_t i, float v, int cm) {
+    if (cm == CM_BF16) {
+        reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
+    } else if (cm == CM_TF32) {
+        reinterpret_cast<float*>(dst)[i] = tf32_round(v);
+    } else if (cm == CM_F32_RAW) {
+        reinterpret_cast<float*>(dst)[i] = v;
+    } else {
+        const float hi = tf32_round(v);
+        reinterpret_cast<float*>(dst)[i] = hi;
+        reinterpret_cast<float*>(dst_lo)[i] = tf32_round(v - hi);
+    }
+}
+
+// ---------------------------------------------------------------- activations
+__global__ void prep_from_nhwc_kernel(const void* __restrict__ src, int bf16, int64_t pixels, int64_t C,
+                                      int64_t Cpad, int cm, void* dst, void* dst_lo) {
+    const int64_t total = pixels * Cpad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pix = i / Cpad, c = i % Cpad;
+        const float v = c < C ? load_as_f32(src, pix * C + c, bf16) : 0.f;
+        store_cm(dst, dst_lo, i, v, cm);
+    }
+}
+
+// 32x32 tile transpose: reads src[n][c][hw] coalesced along hw, writes dst[n][hw][c] along c.
+__global__ void prep_from_nchw_kernel(const void* __restrict__ src, int bf16, int64_t C, int64_t HW, int64_t Cpad,
+                                      int cm, void* dst, void* dst_lo) {
+    __shared__ float tile[32][33];
+    const int64_t n = blockIdx.z;
+    const int64_t hw0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t c = c0 + j, hw = hw0 + tx;
+        float v = 0.f;
+        if (c < C && hw < HW) v = load_as_f32(src, (n * C + c) * HW + hw, bf16);
+        tile[j][tx] = v;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int64_t hw = hw0 + j, c = c0 + tx;
+        if (hw < HW && c < Cpad) store_cm(dst, dst_lo, (n * HW + hw) * Cpad + c, tile[tx][j], cm);
+    }
+}
+
+cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H,
+                              int64_t W, int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
+    const int bf16 = dtype == AI3_BF16;
+    if (in_layout == AI3_NHWC) {
+        const int64_t total = N * H * W * Cpad;
+        const int64_t blocks = (total + 255) / 256;
+        const int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
+        prep_from_nhwc_kernel<<<grid, 256, 0, st>>>(x, bf16, N * H * W, C, Cpad, cm, dst, dst_lo);
+    } else {
+        dim3 grid((unsigned)((H * W + 31) / 32), (unsigned)((Cpad + 31) / 32), (unsigned)N);
+        prep_from_nchw_kernel<<<grid, dim3(32, 8), 0, st>>>(x, bf16, C, H * W, Cpad, cm, dst, dst_lo);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- weights
+__global__ void pack_weights_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t R, int64_t S,
+                                    int64_t Cpad, int cm, void* dst, void* dst_lo) {
+    const int64_t total = K * R * S * Cpad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % Cpad;
+        int64_t t = i / Cpad;
+        const int64_t s = t % S; t /= S;
+        const int64_t r = t % R;
+        const int64_t k = t / R;
+        const float v = c < C ? load_as_f32(w, ((k * C + c) * R + r) * S + s, bf16) : 0.f;
+        store_cm(dst, dst_lo, i, v, cm);
+    }
+}
+
+cudaError_t launch_pack_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
+    const int64_t total = K * R * S * Cpad;
+    const int grid = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+    pack_weights_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, R, S, Cpad, cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
+// U[xi][nu] = sum_{i,j} G[xi][i] g[i][j] G[nu][j],  G = [[1,0,0],[1/2,1/2,1/2],[1/2,-1/2,1/2],[0,0,1]]
+__global__ void winograd_filter_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t Cpad,
+                                       int cm, void* dst, void* dst_lo) {
+    const int64_t total = K * Cpad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / Cpad, c = i % Cpad;
+        float g[3][3];
+        for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) g[r][s] = c < C ? load_as_f32(w, ((k * C + c) * 3 + r) * 3 + s, bf16) : 0.f;
+        float Gg[4][3];  // G g
+        for (int s = 0; s < 3; ++s) {
+            Gg[0][s] = g[0][s];
+            Gg[1][s] = 0.5f * (g[0][s] + g[1][s] + g[2][s]);
+            Gg[2][s] = 0.5f * (g[0][s] - g[1][s] + g[2][s]);
+            Gg[3][s] = g[2][s];
+        }
+        for (int a = 0; a < 4; ++a) {  // (G g) G^T
+            const float u0 = Gg[a][0];
+            const float u1 = 0.5f * (Gg[a][0] + Gg[a][1] + Gg[a][2]);
+            const float u2 = 0.5f * (Gg[a][0] - Gg[a][1] + Gg[a][2]);
+            const float u3 = Gg[a][2];
+            const int64_t plane = K * Cpad;
+            store_cm(dst, dst_lo, (a * 4 + 0) * plane + i, u0, cm);
+            store_cm(dst, dst_lo, (a * 4 + 1) * plane + i, u1, cm);
+            store_cm(dst, dst_lo, (a * 4 + 2) * plane + i, u2, cm);
+            store_cm(dst, dst_lo, (a * 4 + 3) * plane + i, u3, cm);
+        }
+    }
+}
+
+cudaError_t launch_winograd_filter(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t Cpad,
+                                   ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
+    const int64_t total = K * Cpad;
+    const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    winograd_filter_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, Cpad, cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
+__global__ void direct_weights_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t Cg, int64_t R,
+                                      int64_t S, int G, int64_t Kgp, float* __restrict__ dst) {
+    const int64_t Kg = K / G;
+    const int64_t total = (int64_t)G * Cg * R * S * Kgp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t kk = i % Kgp;
+        int64_t t = i / Kgp;
+        const int64_t s = t % S; t /= S;
+        const int64_t r = t % R; t /= R;
+        const int64_t c = t % Cg;
+        const int64_t g = t / Cg;
+        dst[i] = kk < Kg ? load_as_f32(w, (((g * Kg + kk) * Cg + c) * R + r) * S + s, bf16) : 0.f;
+    }
+}
+
+cudaError_t launch_direct_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t Cg, int64_t R, int64_t S,
+                                  int G, int64_t Kgp, float* dst, cudaStream_t st) {
+    const int64_t total = (int64_t)G * Cg * R * S * Kgp;
+    const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    direct_weights_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, Cg, R, S, G, Kgp, dst);
+    return cudaGetLastError();
+}
+
+__global__ void bias_f32_kernel(const void* __restrict__ b, int bf16, int64_t K, float* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = load_as_f32(b, i, bf16);
+}
+
+cudaError_t launch_bias_f32(const void* b, ai3_dtype dtype, int64_t K, float* dst, cudaStream_t st) {
+    bias_f32_kernel<<<(int)((K + 255) / 256), 256, 0, st>>>(b, dtype == AI3_BF16, K, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace ai3

@@ -1,0 +1,55 @@
+"""Shared helpers for the parity tests: run one conv through the C ABI (via the
+Python binding) and through the CPU oracle on the same seeded inputs."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+from synth import ConvShape, conv_inputs
+
+# north_star tolerances on max|err| / max|ref|
+TOL = {("f32", "strict"): 1e-5, ("f32", "tf32"): 1e-3, ("bf16", "strict"): 2e-2, ("bf16", "tf32"): 2e-2}
+WINOGRAD_F32_TOL = 1e-3
+
+
+def tolerance(algo: str, dtype: str, math: str) -> float:
+    if dtype == "f32" and algo == "winograd":
+        return WINOGRAD_F32_TOL
+    return TOL[(dtype, math)]
+
+
+def torch_dtype(dtype: str):
+    return torch.bfloat16 if dtype == "bf16" else torch.float32
+
+
+def to_device(x: np.ndarray, dtype: str, layout: str = "nchw", device="cuda"):
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device=device, dtype=torch_dtype(dtype))
+    if layout == "nhwc":
+        t = t.contiguous(memory_format=torch.channels_last)
+    return t
+
+
+def run_ai3(shape: ConvShape, x, w, b, algo: str, dtype: str, math: str = "strict", layout: str = "nchw",
+            plan: bool = True):
+    """y (fp64 numpy, NCHW) from the GPU path for host arrays x, w, b."""
+    import paper_2410_08300_b200 as ai3
+    xt = to_device(x, dtype, layout)
+    wt = to_device(w, dtype)
+    bt = None if b is None else to_device(b, dtype)
+    if plan:
+        p = ai3.ConvPlan(wt, bt, xt.shape, shape.stride, shape.pad, shape.dil, shape.groups, algo, math,
+                         in_layout=1 if layout == "nhwc" else 0)
+        y = p(xt)
+    else:
+        y = ai3.conv2d(xt, wt, bt, shape.stride, shape.pad, shape.dil, shape.groups, algo, math)
+    torch.cuda.synchronize()
+    return y.float().contiguous().cpu().numpy().astype(np.float64)
+
+
+def ref(shape: ConvShape, x, w, b):
+    return oracle.conv2d(x, w, b, shape.stride, shape.pad, shape.dil, shape.groups)
+
+
+def inputs(shape: ConvShape, seed: int, dtype: str):
+    return conv_inputs(shape, seed, dtype)

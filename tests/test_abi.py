@@ -1,0 +1,143 @@
+"""C ABI tier on the CPU box: libai3.so loads without a GPU, exports every symbol
+include/ai3.h declares, and its host-only entry points (names, output shape,
+support checks, guess, workspace sizing, error reporting) behave as documented.
+No compute call is made here."""
+import ctypes
+import json
+import os
+import re
+
+import pytest
+import torch
+
+import paper_2410_08300_b200 as ai3
+from paper_2410_08300_b200 import _lib
+from synth import workload
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "ai3.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ai3_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    declared = _header_functions()
+    assert len(declared) >= 17
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(_lib.EXPORTS) == declared
+
+
+def test_version_and_names():
+    assert ai3.version() == 1000
+    for name, aid in [("guess", 0), ("default", 0), ("auto", 0), ("direct", 1), ("gemm", 2), ("im2col", 2),
+                      ("implicit_gemm", 3), ("winograd", 4), ("smm", 6), ("custom", 8)]:
+        assert ai3.algo_id(name) == aid
+    assert ai3.algo_name(3) == "implicit_gemm"
+    with pytest.raises(ai3.UnknownAlgorithm, match="unknown algorithm 'fft'"):
+        ai3.algo_id("fft")
+
+
+def test_output_shapes_match_golden():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_examples.json")))
+    for s in g["shapes"]:
+        assert list(ai3.output_shape(s["in"], s["K"], s["kernel"], s["stride"], s["padding"], s["dilation"])) == \
+            s["out"]
+
+
+def test_output_shape_matches_floor_formula_on_workloads():
+    for name in ("vgg16", "resnet50", "alexnet"):
+        for l in workload(name, 2):
+            assert ai3.output_shape((2, l.C, l.H, l.W), l.K, (l.R, l.S), l.stride, l.pad, l.dil) == \
+                (2, l.K, l.P, l.Q)
+
+
+def test_shape_errors_name_the_constraint():
+    with pytest.raises(ai3.Ai3Error, match="larger than the padded input"):
+        ai3.output_shape((1, 3, 2, 2), 4, 3)
+    with pytest.raises(ai3.Ai3Error, match="groups=2 must divide"):
+        ai3.output_shape((1, 3, 8, 8), 4, 3, groups=2)
+    with pytest.raises(ai3.Ai3Error, match="stride"):
+        ai3.output_shape((1, 3, 8, 8), 4, 3, stride=0)
+
+
+def test_winograd_preconditions():
+    base = dict(in_shape=(1, 8, 16, 16), out_channels=8)
+    assert ai3.supported(**base, kernel=3, padding=1, algorithm="winograd")
+    for kw in (dict(kernel=5), dict(kernel=3, stride=2), dict(kernel=3, dilation=2, padding=2)):
+        assert not ai3.supported(**base, **kw, algorithm="winograd")
+    assert not ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="winograd")
+
+
+def test_reserved_algorithms_unsupported():
+    for name in ("smm", "kn2row", "implicit_precomp_gemm", "custom"):
+        with pytest.raises(ai3.UnsupportedConfiguration, match="reserved"):
+            ai3.check_supported((1, 8, 16, 16), 8, 3, algorithm=name)
+
+
+def _all_problem_shapes():
+    out = []
+    for name in ("vgg16", "resnet50", "alexnet", "config1"):
+        out += [(l.N, l.C, l.H, l.W, l.K, l.R, l.stride, l.pad, l.dil, 1) for l in workload(name, 2)]
+    out += [(2, 8, 9, 9, 8, 3, 1, 1, 1, 2), (1, 4, 5, 5, 4, 1, 1, 0, 1, 4), (3, 6, 12, 10, 9, 5, 2, 2, 2, 3)]
+    return out
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_guess_is_deterministic_and_supported(dtype):
+    """guess never returns an algorithm whose preconditions the spec violates."""
+    for (N, C, H, W, K, R, s, p, d, g) in _all_problem_shapes():
+        a = ai3.guess((N, C, H, W), K, R, s, p, d, g, dtype=dtype)
+        assert a == ai3.guess((N, C, H, W), K, R, s, p, d, g, dtype=dtype)
+        assert a in ("direct", "gemm", "implicit_gemm", "winograd")
+        assert ai3.supported((N, C, H, W), K, R, s, p, d, g, dtype=dtype, algorithm=a)
+        if g > 1:
+            assert a == "direct"
+
+
+def test_workspace_sizes():
+    lib = _lib.load()
+
+    def ws(shape, K, R, algo, dtype=_lib.BF16, math=_lib.MATH_STRICT, lin=_lib.NHWC, lout=_lib.NHWC, pad=1):
+        prm = _lib.params(K, (R, R), (1, 1), (pad, pad), (1, 1), 1, True)
+        out = ctypes.c_size_t()
+        st = lib.ai3_conv2d_workspace_size(ctypes.byref(prm), _lib.shape4(shape), dtype, math, ai3.algo_id(algo),
+                                           lin, lout, ctypes.byref(out))
+        assert st == 0, _lib.last_error()
+        return out.value
+
+    # implicit GEMM on NHWC bf16 with C % 16 == 0: only the prepared weights (K*R*S*C*2 + bias)
+    w_only = ws((64, 256, 56, 56), 256, 3, "implicit_gemm")
+    assert w_only == 256 * 9 * 256 * 2 + 256 * 4
+    # explicit GEMM adds the im2col matrix
+    assert ws((64, 256, 56, 56), 256, 3, "gemm") >= w_only + 64 * 56 * 56 * 9 * 256 * 2
+    # NCHW input adds the layout pass
+    assert ws((64, 256, 56, 56), 256, 3, "implicit_gemm", lin=_lib.NCHW) >= w_only + 64 * 56 * 56 * 256 * 2
+    # Winograd: 16 transformed tiles in (V) and out (M, fp32)
+    T = 64 * 28 * 28
+    assert ws((64, 256, 56, 56), 256, 3, "winograd") >= 16 * T * 256 * 2 + 16 * T * 256 * 4
+    # direct needs no workspace beyond the fp32 weights
+    # direct: fp32 weights [Cg][R][S][K padded to 32] + fp32 bias, each region 256-byte aligned
+    assert ws((2, 3, 32, 32), 16, 3, "direct", dtype=_lib.F32) == 3584 + 256
+
+
+def test_null_and_bad_arguments():
+    lib = _lib.load()
+    out = (ctypes.c_int64 * 4)()
+    assert lib.ai3_conv2d_output_shape(None, _lib.shape4((1, 1, 4, 4)), out) == _lib.ERR_INVALID_ARGUMENT
+    assert "null" in _lib.last_error()
+    assert lib.ai3_conv2d_plan_execute(None, None, None, None, 0, None) == _lib.ERR_INVALID_ARGUMENT
+    lib.ai3_conv2d_plan_destroy(None)  # no-op
+
+
+def test_product_never_imports_oracle():
+    """The product package must not route through the oracle (there is no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2410_08300_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), fn

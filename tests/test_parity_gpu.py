@@ -1,0 +1,193 @@
+"""GPU parity: every algorithm, through the C ABI, against the CPU fp64 oracle on
+the same seeded inputs (tolerances are the north_star's, see helpers.TOL).
+
+Sizes span several 128-row tiles with a ragged tail; integer-valued cases must be
+bit-exact; full-size layers are checked on sampled outputs in tests/test_fullsize_gpu.py.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from helpers import inputs, ref, run_ai3, tolerance, to_device
+from synth import CONFIG1, ConvShape, integer_inputs
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ["direct", "gemm", "implicit_gemm", "winograd", "guess"]
+MODES = [("f32", "strict"), ("f32", "tf32"), ("bf16", "strict")]
+
+
+def _supports(shape: ConvShape, algo: str) -> bool:
+    if algo in ("direct", "guess"):
+        return True
+    if shape.groups != 1:
+        return False
+    if algo == "winograd":
+        return shape.R == 3 and shape.S == 3 and shape.stride == 1 and shape.dil == 1
+    return True
+
+
+def _check(shape, algo, dtype, math, layout, seed, plan=True):
+    x, w, b = inputs(shape, seed, dtype)
+    y = run_ai3(shape, x, w, b, algo, dtype, math, layout, plan)
+    r = ref(shape, x, w, b)
+    err = oracle.rel_err(y, r)
+    tol = tolerance(algo, dtype, math)
+    assert err <= tol, f"{algo} {dtype}/{math} {layout}: rel err {err:.3e} > {tol:.0e}"
+    return err
+
+
+# ------------------------------------------------------------------ config 1 (BASELINE configs[0])
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype,math", MODES)
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+def test_config1_all_algorithms(algo, dtype, math, layout):
+    _check(CONFIG1, algo, dtype, math, layout, seed=1000)
+
+
+def test_config1_stateless_call():
+    for algo in ALGOS:
+        _check(CONFIG1, algo, "f32", "strict", "nchw", seed=1001, plan=False)
+
+
+# ------------------------------------------------------------------ multi-tile ragged shapes
+RAGGED = [
+    ConvShape("r3x3", 2, 64, 23, 23, 96, 3, 3, 1, 1),     # M = 1058: 9 tiles, 34-row tail
+    ConvShape("r3x3_c48", 3, 48, 17, 19, 40, 3, 3, 1, 1),  # C not a multiple of 64, K < 64
+    ConvShape("r3x3_k200", 1, 128, 30, 30, 200, 3, 3, 1, 1, bias=False),
+    ConvShape("r1x1", 2, 256, 14, 14, 72, 1, 1),
+    ConvShape("r1x1s2", 2, 96, 15, 15, 64, 1, 1, 2, 0),
+    ConvShape("r5x5", 2, 32, 21, 20, 48, 5, 5, 1, 2),
+    ConvShape("r7x7s2", 2, 3, 45, 45, 64, 7, 7, 2, 3),     # ResNet stem shape, small
+    ConvShape("r11s4", 2, 3, 67, 67, 64, 11, 11, 4, 2),    # AlexNet conv1 shape, small
+    ConvShape("r3x3d2", 2, 32, 19, 19, 32, 3, 3, 1, 2, 2),
+    ConvShape("r3x3s2", 2, 128, 28, 28, 128, 3, 3, 2, 1),
+    ConvShape("rodd", 1, 16, 9, 7, 24, 3, 3, 1, 0),       # odd P, Q: Winograd crop
+]
+
+
+@pytest.mark.parametrize("shape", RAGGED, ids=lambda s: s.name)
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype,math", MODES)
+def test_ragged_shapes(shape, algo, dtype, math):
+    if not _supports(shape, algo):
+        pytest.skip("algorithm precondition")
+    _check(shape, algo, dtype, math, "nhwc" if shape.C % 2 == 0 else "nchw", seed=hash(shape.name) & 0xFFFF)
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("algo", ["implicit_gemm", "gemm", "winograd", "direct"])
+def test_layouts_bf16(layout, algo):
+    _check(RAGGED[0], algo, "bf16", "strict", layout, seed=7)
+
+
+# ------------------------------------------------------------------ SPEC sweep ranges
+def _sweep(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        R = int(rng.integers(1, 6)); S = int(rng.integers(1, 6))
+        st = int(rng.integers(1, 4)); pd = int(rng.integers(0, 3)); dl = int(rng.integers(1, 3))
+        G = int(rng.integers(1, 3)) if len(out) % 3 == 0 else 1
+        C = G * int(rng.integers(1, 9)); K = G * int(rng.integers(1, 9))
+        H = int(rng.integers(4, 17)); W = int(rng.integers(4, 17)); N = int(rng.integers(1, 5))
+        if H + 2 * pd < dl * (R - 1) + 1 or W + 2 * pd < dl * (S - 1) + 1:
+            continue
+        out.append(ConvShape(f"sw{len(out)}", N, C, H, W, K, R, S, st, pd, dl, G, bias=bool(rng.integers(0, 2))))
+    # make sure Winograd-eligible shapes are in the sweep
+    out += [ConvShape(f"sww{i}", int(rng.integers(1, 5)), int(rng.integers(1, 9)), int(rng.integers(4, 17)),
+                      int(rng.integers(4, 17)), int(rng.integers(1, 9)), 3, 3, 1, int(rng.integers(0, 3)))
+            for i in range(6)]
+    return out
+
+
+@pytest.mark.parametrize("shape", _sweep(24, 42), ids=lambda s: s.name)
+@pytest.mark.parametrize("algo", ALGOS)
+def test_spec_sweep(shape, algo):
+    if not _supports(shape, algo):
+        pytest.skip("algorithm precondition")
+    for dtype, math in (("f32", "strict"), ("bf16", "strict")):
+        _check(shape, algo, dtype, math, "nchw", seed=hash((shape.name, algo)) & 0xFFFF)
+
+
+# ------------------------------------------------------------------ exact cases
+INT_SHAPES = [ConvShape("i3x3", 2, 64, 20, 21, 80, 3, 3, 1, 1), ConvShape("i5x5s2", 2, 16, 19, 17, 32, 5, 5, 2, 2),
+              ConvShape("i1x1", 3, 32, 11, 13, 48, 1, 1), ConvShape("i3x3c3", 2, 3, 33, 31, 16, 3, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("shape", INT_SHAPES, ids=lambda s: s.name)
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype,math", MODES)
+def test_integer_inputs_bit_exact(shape, algo, dtype, math):
+    """Integer x, w, b keep every product and partial sum exact in fp32 (and every
+    operand exact in tf32 / bf16), so each path must reproduce the oracle bit for bit.
+    bf16 outputs additionally need |y| <= 256: use x, w in {-1, 0, 1} there."""
+    if not _supports(shape, algo):
+        pytest.skip("algorithm precondition")
+    small = dtype == "bf16"
+    x, w, b = integer_inputs(shape, seed=5, xmax=1 if small else 8, wmax=1 if small else 4)
+    if small and shape.C * shape.R * shape.S > 250:
+        x, w = x, w * (np.abs(np.arange(w.size).reshape(w.shape) % 3) == 0)  # thin out taps to keep |y| <= 256
+    y = run_ai3(shape, x, w, b, algo, dtype, math, "nhwc")
+    r = ref(shape, x, w, b)
+    assert np.abs(r).max() < (256 if small else 2 ** 24)
+    np.testing.assert_array_equal(y, r)
+
+
+# ------------------------------------------------------------------ degenerate cases
+DEGEN = [ConvShape("out1x1", 2, 8, 3, 3, 5, 3, 3), ConvShape("k1", 1, 4, 6, 6, 1, 3, 3, 1, 1),
+         ConvShape("c1", 2, 1, 9, 9, 16, 3, 3, 1, 1), ConvShape("hw1", 3, 32, 1, 1, 24, 1, 1),
+         ConvShape("pad_only", 1, 2, 1, 1, 3, 3, 3, 1, 1), ConvShape("wide", 1, 8, 2, 130, 8, 1, 3, 1, 0)]
+
+
+@pytest.mark.parametrize("shape", DEGEN, ids=lambda s: s.name)
+@pytest.mark.parametrize("algo", ALGOS)
+def test_degenerate(shape, algo):
+    if not _supports(shape, algo):
+        pytest.skip("algorithm precondition")
+    _check(shape, algo, "f32", "strict", "nchw", seed=3)
+    _check(shape, algo, "bf16", "strict", "nhwc", seed=4)
+
+
+# ------------------------------------------------------------------ determinism / batch independence
+@pytest.mark.parametrize("algo", ["direct", "gemm", "implicit_gemm", "winograd"])
+def test_deterministic_and_batch_independent(algo):
+    """Same plan + input -> identical bits; and image n's output does not depend on the
+    batch it was computed in (pins that batch sharding across GPUs is exact)."""
+    import paper_2410_08300_b200 as ai3
+    shape = ConvShape("det", 6, 64, 19, 19, 64, 3, 3, 1, 1)
+    x, w, b = inputs(shape, 11, "bf16")
+    xt, wt, bt = to_device(x, "bf16", "nhwc"), to_device(w, "bf16"), to_device(b, "bf16")
+    p = ai3.ConvPlan(wt, bt, xt.shape, 1, 1, 1, 1, algo, in_layout=1)
+    y1, y2 = p(xt).clone(), p(xt).clone()
+    assert torch.equal(y1, y2)
+    p2 = ai3.ConvPlan(wt, bt, (2,) + tuple(xt.shape[1:]), 1, 1, 1, 1, algo, in_layout=1)
+    for s in (0, 2, 4):
+        part = p2(xt[s:s + 2].contiguous(memory_format=torch.channels_last))
+        assert torch.equal(part, y1[s:s + 2])
+
+
+# ------------------------------------------------------------------ the harness has teeth
+def test_mutation_dropped_bias_is_caught():
+    shape = ConvShape("mut", 2, 16, 12, 12, 24, 3, 3, 1, 1)
+    x, w, b = inputs(shape, 9, "f32")
+    y = run_ai3(shape, x, w, b, "implicit_gemm", "f32", "strict", "nchw")
+    r = ref(shape, x, w, b)
+    mutated = y - b.astype(np.float64)[None, :, None, None]
+    assert oracle.rel_err(y, r) <= 1e-5
+    assert oracle.rel_err(mutated, r) > 1e-3
+
+
+def test_errors_surface_as_exceptions():
+    import paper_2410_08300_b200 as ai3
+    x = torch.zeros(1, 3, 8, 8, device="cuda")
+    w = torch.zeros(4, 3, 5, 5, device="cuda")
+    with pytest.raises(ai3.UnsupportedConfiguration):
+        ai3.conv2d(x, w, None, 1, 0, 1, 1, "winograd")
+    with pytest.raises(ai3.UnknownAlgorithm):
+        ai3.conv2d(x, w, None, 1, 0, 1, 1, "nope")
+    with pytest.raises(ai3.Ai3Error):
+        ai3.conv2d(x, torch.zeros(4, 3, 9, 9, device="cuda"), None)  # kernel larger than input
