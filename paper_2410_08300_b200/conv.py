@@ -254,7 +254,8 @@ class ConvPlan:
             raise ValueError(f"plan built for {self.in_shape} {self.dtype}, got {tuple(x.shape)} {x.dtype}")
         if x.device != self.device:
             raise ValueError("input on a different device than the plan")
-        if layout_of(x) != self.in_layout:
+        fmt = torch.channels_last if self.in_layout == _lib.NHWC else torch.contiguous_format
+        if not x.is_contiguous(memory_format=fmt):
             raise ValueError("input memory format differs from the plan's")
         if out is None:
             fmt = torch.channels_last if self.out_layout == _lib.NHWC else torch.contiguous_format

@@ -22,7 +22,7 @@ __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
 }  // namespace
 
 template <int KS>
-__global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp) {
+__global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp, int xs_floats) {
     extern __shared__ float smem[];
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
     const int ih0 = p0 * a.sh - a.ph, iw0 = q0 * a.sw - a.pw;
 
     float* xs = smem;                         // [CB][FH][FWp]
-    float* ws = smem + (size_t)CB * FH * FWp;  // [CB][R][S][TK]
+    float* ws = smem + xs_floats;  // [CB][R][S][TK], 16-byte aligned for float4 loads
 
     float acc[8][4];
 #pragma unroll
@@ -126,13 +126,14 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
     int CB = budget / per_c;
     if (CB < 1) CB = 1;
     if (CB > a.Cg) CB = a.Cg;
-    const size_t smem = (size_t)CB * per_c;
+    const int xs_floats = (CB * FH * FWp + 3) / 4 * 4;
+    const size_t smem = (size_t)xs_floats * 4 + (size_t)CB * a.R * a.S * TK * 4;
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
     dim3 grid(tiles, (unsigned)((a.Kg + TK - 1) / TK), (unsigned)(a.N * a.G));
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp);
+        kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp, xs_floats);
     };
     if (a.R == a.S && a.R == 3) launch(direct_conv_kernel<3>);
     else if (a.R == a.S && a.R == 1) launch(direct_conv_kernel<1>);

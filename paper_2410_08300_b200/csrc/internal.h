@@ -84,6 +84,7 @@ struct TcArgs {
     int block_n;    // 32 / 64 / 128 / 256
     int row_bytes;  // 32 / 64 / 128: bytes of one K-block row (swizzle width)
     int num_kb;     // K-blocks per tile
+    int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
     int m_tiles, n_tiles;
     // im2col coordinates (a_mode == TC_A_IM2COL)

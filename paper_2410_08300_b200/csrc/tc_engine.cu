@@ -39,6 +39,44 @@ constexpr int NUM_THREADS = 192;
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 }  // namespace
 
+// Store one row's 32 consecutive output channels (col0..col0+31) of a tile: + bias (fp32),
+// cast, and write NHWC-contiguous (vectorised) or NCHW (strided by P*Q; a warp's 32 rows
+// are 32 consecutive pixels, so each column store coalesces).
+__device__ __forceinline__ void epilogue_store(const TcArgs& a, float (&f)[32], int64_t base, int64_t cstride,
+                                               int col0) {
+    if (col0 >= a.Ncols) return;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int col = col0 + j;
+        f[j] += (a.bias && col < a.Ncols) ? a.bias[col] : 0.f;
+    }
+    const bool full_chunk = col0 + 32 <= a.Ncols;
+    if (!a.out_nchw && full_chunk && a.out_bf16 && (a.Ncols % 8) == 0) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + base + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            __nv_bfloat162 h[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+            dst[q] = *reinterpret_cast<uint4*>(h);
+        }
+    } else if (!a.out_nchw && full_chunk && !a.out_bf16 && (a.Ncols % 4) == 0) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + base + col0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int col = col0 + j;
+            if (col < a.Ncols) {
+                const int64_t o = base + (int64_t)col * cstride;
+                if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(f[j]);
+                else reinterpret_cast<float*>(a.out)[o] = f[j];
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                    const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1, const TcArgs a,
@@ -121,41 +159,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        // The K loop of a tile is split into accumulation chunks of `promote_kb` K-blocks
+        // (the whole loop unless 3xTF32); each chunk goes to one of the two TMEM buffers
+        // and is handed to the epilogue, which for 3xTF32 sums the chunks in fp32
+        // registers (the tensor-core accumulator alone drifts ~7.5e-9 x K).
         if (elect_one()) {
             const uint32_t idesc = make_idesc(BM, a.block_n, a.cm == CM_BF16 ? 1u : 2u);
             const int kslices = a.row_bytes / 32;
+            const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * a.block_n;
+                uint32_t d_tmem = 0;
                 for (int kb = 0; kb < a.num_kb; ++kb) {
+                    const int kc = kb % pk;  // position inside the accumulation chunk
+                    if (kc == 0) {
+                        mbar_wait(&tempty[acc], acc_phase ^ 1);
+                        tc_fence_after();
+                        d_tmem = tmem_base + acc * a.block_n;
+                    }
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sA = smem_u32(smem + stage * stage_bytes);
                     const uint32_t sB = sA + splits * a_bytes;
                     for (int k = 0; k < kslices; ++k) {
-                        const uint32_t first = (kb | k) != 0;
+                        const uint32_t accumulate = (kc | k) != 0;
                         const uint64_t ad = make_sdesc(sA + k * 32, a.row_bytes);
                         const uint64_t bd = make_sdesc(sB + k * 32, a.row_bytes);
                         if (a.cm == CM_BF16) {
-                            mma_bf16(d_tmem, ad, bd, idesc, first);
+                            mma_bf16(d_tmem, ad, bd, idesc, accumulate);
                         } else if (a.cm == CM_TF32) {
-                            mma_tf32(d_tmem, ad, bd, idesc, first);
+                            mma_tf32(d_tmem, ad, bd, idesc, accumulate);
                         } else {
                             const uint64_t ad_lo = make_sdesc(sA + a_bytes + k * 32, a.row_bytes);
                             const uint64_t bd_lo = make_sdesc(sB + b_bytes + k * 32, a.row_bytes);
-                            mma_tf32(d_tmem, ad_lo, bd, idesc, first);
+                            mma_tf32(d_tmem, ad_lo, bd, idesc, accumulate);
                             mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
                             mma_tf32(d_tmem, ad, bd, idesc, 1u);
                         }
                     }
                     mma_commit(&empty[stage]);
                     if (++stage == a.stages) { stage = 0; phase ^= 1; }
+                    if (kc == pk - 1 || kb == a.num_kb - 1) {
+                        mma_commit(&tfull[acc]);
+                        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                    }
                 }
-                mma_commit(&tfull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
         __syncwarp();
@@ -163,6 +212,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ------------------------------------------------------------ epilogue (warps 2..5)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int row = quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
+        const int nchunks = (a.num_kb + pk - 1) / pk;
+        const int ncol32 = a.block_n / 32;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -181,51 +234,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 base = ob + (int64_t)m * a.Ncols;
                 cstride = 1;
             }
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            for (int chunk = 0; chunk < a.block_n / 32; ++chunk) {
-                uint32_t v[32];
-                tmem_ld32(tmem_base + acc * a.block_n + chunk * 32 + ((uint32_t)(quarter * 32) << 16), v);
-                tmem_ld_wait();
-                const int col0 = n0 + chunk * 32;
-                if (!row_ok || col0 >= a.Ncols) continue;
-                float f[32];
+            if (nchunks == 1) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                for (int c32 = 0; c32 < ncol32; ++c32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem_base + acc * a.block_n + c32 * 32 + lane_off, v);
+                    tmem_ld_wait();
+                    float f[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int col = col0 + j;
-                    const float bv = (a.bias && col < a.Ncols) ? a.bias[col] : 0.f;
-                    f[j] = __uint_as_float(v[j]) + bv;
+                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                    if (row_ok) epilogue_store(a, f, base, cstride, n0 + c32 * 32);
                 }
-                const bool full_chunk = col0 + 32 <= a.Ncols;
-                if (!a.out_nchw && full_chunk && a.out_bf16 && (a.Ncols % 8) == 0) {
-                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + base + col0);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            } else {
+                // 3xTF32: sum the per-chunk tensor-core partials in fp32 registers (block_n <= 128)
+                float racc[4][32];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        __nv_bfloat162 h[4];
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
-                        dst[q] = *reinterpret_cast<uint4*>(h);
-                    }
-                } else if (!a.out_nchw && full_chunk && !a.out_bf16 && (a.Ncols % 4) == 0) {
-                    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + base + col0);
+                    for (int j = 0; j < 32; ++j) racc[c][j] = 0.f;
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
-                } else {
+                    for (int c = 0; c < 4; ++c) {
+                        if (c < ncol32) {
+                            uint32_t v[32];
+                            tmem_ld32(tmem_base + acc * a.block_n + c * 32 + lane_off, v);
+                            tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = col0 + j;
-                        if (col < a.Ncols) {
-                            const int64_t o = base + (int64_t)col * cstride;
-                            if (a.out_bf16) reinterpret_cast<__nv_bfloat16*>(a.out)[o] = __float2bfloat16_rn(f[j]);
-                            else reinterpret_cast<float*>(a.out)[o] = f[j];
+                            for (int j = 0; j < 32; ++j) racc[c][j] += __uint_as_float(v[j]);
                         }
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                }
+                if (row_ok) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c < ncol32) epilogue_store(a, racc[c], base, cstride, n0 + c * 32);
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
@@ -258,6 +313,8 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.block_n == 0) a.block_n = pick_block_n(a.Ncols);
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
     if (a.cm == CM_3XTF32 && a.block_n > 128) a.block_n = 128;
+    // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
+    a.promote_kb = a.cm == CM_3XTF32 ? (256 / (a.row_bytes / 4) > 0 ? 256 / (a.row_bytes / 4) : 1) : 0;
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const int stage_bytes = splits * (BM + a.block_n) * a.row_bytes;
     const int reserve = 1024 /* barriers */ + 1024 /* alignment slack */;

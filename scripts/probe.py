@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import oracle
 from synth import ConvShape, conv_inputs
-from tests.helpers import run_ai3, ref, tolerance
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from helpers import run_ai3, ref, tolerance
 
 algo = sys.argv[1]
 SHAPES = [(1, 3, 32, 32, 16, 3, 3, 1, 1), (2, 64, 23, 23, 96, 3, 3, 1, 1), (2, 3, 45, 45, 64, 7, 7, 2, 3),
