@@ -198,6 +198,8 @@ struct ai3_plan {
     std::mutex mu;
     const void* cached_a_src = nullptr;
     CUtensorMap ta0{}, ta1{};
+    const void* cached_out = nullptr;
+    CUtensorMap tout{};
     int launches = 1;
 };
 
@@ -308,6 +310,10 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         pl.launches = (pl.need_prep ? 1 : 0) + 3;
     }
     pl.ws_bytes = ws;
+    // TMA-store epilogue for row-major (NHWC / [b][T][K]) outputs whose rows are 16-byte multiples
+    const int eo = a.out_bf16 ? 2 : 4;
+    a.stg_row = (!a.out_nchw && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
+    a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
     return ok();
 }
@@ -325,14 +331,14 @@ ai3_status encode_b_maps(ai3_plan& pl) {
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         const uint64_t dims[3] = {(uint64_t)pl.Cpad, (uint64_t)c.K, 16};
         const uint64_t str[2] = {(uint64_t)pl.Cpad * pl.elem, (uint64_t)c.K * pl.Cpad * pl.elem};
-        const uint32_t box[3] = {kel, (uint32_t)a.block_n, 1};
+        const uint32_t box[3] = {kel, (uint32_t)(a.block_n / a.cg), 1};
         okb = encode_tiled(&pl.tb0, dt, 3, w, dims, str, box, sw);
         if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 3, wlo, dims, str, box, sw);
     } else {
         const uint64_t kred = (uint64_t)(c.R * c.S * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
         const uint64_t str[1] = {kred * pl.elem};
-        const uint32_t box[2] = {kel, (uint32_t)a.block_n};
+        const uint32_t box[2] = {kel, (uint32_t)(a.block_n / a.cg)};
         okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box, sw);
         if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 2, wlo, dims, str, box, sw);
     }
@@ -380,6 +386,33 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
     }
     if (pl.splits != 2) pl.ta1 = pl.ta0;
     pl.cached_a_src = src;
+    return ok();
+}
+
+// Encode (or reuse) the output tensor map of the TMA-store epilogue for destination `out`.
+ai3_status encode_out_map(ai3_plan& pl, void* out) {
+    const TcArgs& a = pl.tc.args;
+    if (a.stg_row == 0 || pl.cached_out == out) return ok();
+    const int eo = a.out_bf16 ? 2 : 4;
+    const CUtensorMapDataType dt = a.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapSwizzle sw = a.stg_row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+    bool okm;
+    if (a.batch > 1) {
+        const uint64_t dims[3] = {(uint64_t)a.Ncols, (uint64_t)a.M, (uint64_t)a.batch};
+        const uint64_t str[2] = {(uint64_t)a.Ncols * eo, (uint64_t)a.out_bstride * eo};
+        const uint32_t box[3] = {32, 32, 1};
+        okm = encode_tiled(&pl.tout, dt, 3, out, dims, str, box, sw);
+    } else {
+        const uint64_t dims[2] = {(uint64_t)a.Ncols, (uint64_t)a.M};
+        const uint64_t str[1] = {(uint64_t)a.Ncols * eo};
+        const uint32_t box[2] = {32, 32};
+        okm = encode_tiled(&pl.tout, dt, 2, out, dims, str, box, sw);
+    }
+    if (!okm) {
+        pl.cached_out = nullptr;
+        return fail(AI3_ERR_CUDA, "tensor-map encoding failed for the output (%s)", ai3_algo_name(pl.algo));
+    }
+    pl.cached_out = out;
     return ok();
 }
 
@@ -461,7 +494,9 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.out = w + pl.ws_M;
         tp.args.bias = nullptr;
     }
-    e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, st);
+    if (tp.args.stg_row && !aligned(tp.args.out, 16)) tp.args.stg_row = 0;  // TMA needs a 16-byte base
+    if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
+    e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,

@@ -86,6 +86,8 @@ struct TcArgs {
     int num_kb;     // K-blocks per tile
     int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
+    int dbg;        // 0 normal; 1 = no MMA (TMA pipeline only); 2 = no TMA (MMA on stale smem); 3 = no epilogue stores -- timing probes
+    int cg;         // CTAs per MMA group: 1 or 2 (cta_group::2 pair, 256-row tiles)
     int m_tiles, n_tiles;
     // im2col coordinates (a_mode == TC_A_IM2COL)
     int Q, PQ, sh, sw, ph, pw, dh, dw, S, c_chunks;
@@ -93,6 +95,9 @@ struct TcArgs {
     int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
     int out_bf16;
     int epi_PQ;
+    int stg_row;    // TMA-store epilogue: bytes per staged row (32 * out elem); 0 = direct stores
+    int bias_smem;  // 1: the epilogue stages the fp32 bias in shared memory
+    int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
     const float* bias;  // fp32 [Ncols] or null
     void* out;
     long long out_bstride;  // elements between batches
@@ -110,7 +115,7 @@ struct TcPlan {
 void tc_configure(TcPlan& p, int num_sms);
 // Encode the tensor maps and launch.  a0/a1/b0/b1 are prepared by the caller.
 cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b0,
-                      const CUtensorMap* b1, cudaStream_t st);
+                      const CUtensorMap* b1, const CUtensorMap* out, cudaStream_t st);
 
 // Driver entry points for tensor-map encoding (resolved once via cudaGetDriverEntryPoint).
 bool encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* addr, const uint64_t* dims,

@@ -27,6 +27,7 @@
 // 3xTF32 (strict fp32): per K slice acc += A_lo B_hi + A_hi B_lo + A_hi B_hi.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <mutex>
 #include "internal.h"
 #include "ptx.cuh"
@@ -43,12 +44,14 @@ constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 // cast, and write NHWC-contiguous (vectorised) or NCHW (strided by P*Q; a warp's 32 rows
 // are 32 consecutive pixels, so each column store coalesces).
 __device__ __forceinline__ void epilogue_store(const TcArgs& a, float (&f)[32], int64_t base, int64_t cstride,
-                                               int col0) {
+                                               int col0, bool bias_added = false) {
     if (col0 >= a.Ncols) return;
+    if (!bias_added) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        f[j] += (a.bias && col < a.Ncols) ? a.bias[col] : 0.f;
+        for (int j = 0; j < 32; ++j) {
+            const int col = col0 + j;
+            f[j] += (a.bias && col < a.Ncols) ? a.bias[col] : 0.f;
+        }
     }
     const bool full_chunk = col0 + 32 <= a.Ncols;
     if (!a.out_nchw && full_chunk && a.out_bf16 && (a.Ncols % 8) == 0) {
@@ -77,17 +80,188 @@ __device__ __forceinline__ void epilogue_store(const TcArgs& a, float (&f)[32], 
     }
 }
 
+// ---------------------------------------------------------------- TMA producer (one thread)
+// Walks the K-blocks of every tile of this CTA group and streams A/B tiles into the smem
+// ring.  Filter-tap / channel-chunk coordinates advance incrementally (no division in
+// the K loop).  For a CTA pair both CTAs' bytes complete on the leader's full barrier.
+template <int CG>
+__device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0, const CUtensorMap& ta1,
+                                         const CUtensorMap& tb0, const CUtensorMap& tb1, uint8_t* smem,
+                                         uint64_t* full, uint64_t* empty, uint32_t rank, int unit, int num_units) {
+    const bool leader = rank == 0;
+    const int splits = a.cm == CM_3XTF32 ? 2 : 1;
+    const int bn_cta = a.block_n / CG;
+    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
+    const int tiles_per_batch = a.m_tiles * a.n_tiles;
+    const int total_tiles = tiles_per_batch * a.batch;
+    const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = unit; tile < total_tiles; tile += num_units) {
+        const int b = tile / tiles_per_batch;
+        const int rem = tile - b * tiles_per_batch;
+        const int mt = rem / a.n_tiles;
+        const int m0 = mt * (BM * CG) + (int)rank * BM;
+        const int n0 = (rem - mt * a.n_tiles) * a.block_n + (int)rank * bn_cta;
+        int n_img = 0, hbase = 0, wbase = 0;
+        if (a.a_mode == TC_A_IM2COL) {
+            n_img = m0 / a.PQ;
+            const int pq = m0 - n_img * a.PQ;
+            const int p = pq / a.Q;
+            hbase = p * a.sh - a.ph;
+            wbase = (pq - p * a.Q) * a.sw - a.pw;
+        }
+        int cc = 0, ts = 0, tr = 0;  // channel chunk, filter column, filter row of the current K-block
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sA = smem + stage * stage_bytes;
+            uint8_t* sB = sA + splits * a_bytes;
+            const int kx = kb * kelems;
+            if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
+                if (leader) mbar_arrive(&full[stage]);
+            } else if (CG == 1) {
+                uint64_t* bar = &full[stage];
+                mbar_arrive_expect_tx(bar, stage_bytes);
+                if (a.a_mode == TC_A_IM2COL) {
+                    const uint16_t ow = (uint16_t)(ts * a.dw), oh = (uint16_t)(tr * a.dh);
+                    tma_load_im2col_4d(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    if (splits == 2) tma_load_im2col_4d(sA + a_bytes, &ta1, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    tma_load_2d(sB, &tb0, bar, kx, n0);
+                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, bar, kx, n0);
+                } else if (a.a_mode == TC_A_TILED2D) {
+                    tma_load_2d(sA, &ta0, bar, kx, m0);
+                    if (splits == 2) tma_load_2d(sA + a_bytes, &ta1, bar, kx, m0);
+                    tma_load_2d(sB, &tb0, bar, kx, n0);
+                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, bar, kx, n0);
+                } else {
+                    tma_load_3d(sA, &ta0, bar, kx, m0, b);
+                    if (splits == 2) tma_load_3d(sA + a_bytes, &ta1, bar, kx, m0, b);
+                    tma_load_3d(sB, &tb0, bar, kx, n0, b);
+                    if (splits == 2) tma_load_3d(sB + b_bytes, &tb1, bar, kx, n0, b);
+                }
+            } else {
+                if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+                const uint32_t bar = full_base + stage * 8;
+                if (a.a_mode == TC_A_IM2COL) {
+                    const uint16_t ow = (uint16_t)(ts * a.dw), oh = (uint16_t)(tr * a.dh);
+                    tma_load_im2col_4d_cg2(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    if (splits == 2) tma_load_im2col_4d_cg2(sA + a_bytes, &ta1, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
+                    if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kx, n0);
+                } else if (a.a_mode == TC_A_TILED2D) {
+                    tma_load_2d_cg2(sA, &ta0, bar, kx, m0);
+                    if (splits == 2) tma_load_2d_cg2(sA + a_bytes, &ta1, bar, kx, m0);
+                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
+                    if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kx, n0);
+                } else {
+                    tma_load_3d_cg2(sA, &ta0, bar, kx, m0, b);
+                    if (splits == 2) tma_load_3d_cg2(sA + a_bytes, &ta1, bar, kx, m0, b);
+                    tma_load_3d_cg2(sB, &tb0, bar, kx, n0, b);
+                    if (splits == 2) tma_load_3d_cg2(sB + b_bytes, &tb1, bar, kx, n0, b);
+                }
+            }
+            if (++cc == a.c_chunks) { cc = 0; if (++ts == a.S) { ts = 0; ++tr; } }
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- MMA issuer (one thread)
+// The K loop of a tile is split into accumulation chunks of `promote_kb` K-blocks (the
+// whole loop unless 3xTF32); each chunk goes to one of the two TMEM buffers and is handed
+// to the epilogue, which for 3xTF32 sums the chunks in fp32 registers (the tensor-core
+// accumulator alone drifts ~7.5e-9 x K).  Descriptors are built once and
+// advanced by adding byte offsets >> 4 (K slice: +32 B, stage: +stage_bytes).
+template <int CG, int CMODE, int KS>
+__device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                           uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base, int unit,
+                                           int num_units) {
+    constexpr int splits = CMODE == CM_3XTF32 ? 2 : 1;
+    const int bn_cta = a.block_n / CG;
+    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const uint32_t idesc = make_idesc(BM * CG, a.block_n, CMODE == CM_BF16 ? 1u : 2u);
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t a_desc0 = make_sdesc(s0, a.row_bytes);
+    const uint64_t b_desc0 = make_sdesc(s0 + splits * a_bytes, a.row_bytes);
+    const uint64_t alo_off = a_bytes >> 4, blo_off = b_bytes >> 4;
+    const int tiles = a.m_tiles * a.n_tiles * a.batch;
+    const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
+    const bool no_mma = a.dbg == 1;
+    int stage = 0, acc = 0, kc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    uint32_t d_tmem = tmem_base;
+    for (int tile = unit; tile < tiles; tile += num_units) {
+        kc = 0;
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+            if (kc == 0) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                d_tmem = tmem_base + acc * a.block_n;
+            }
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t soff = (uint64_t)((stage * stage_bytes) >> 4);
+            const uint64_t ad = a_desc0 + soff, bd = b_desc0 + soff;
+            if (!no_mma) {
+#pragma unroll
+                for (int k = 0; k < KS; ++k) {
+                    const uint32_t accum = (k > 0 || kc > 0) ? 1u : 0u;
+                    const uint64_t adk = ad + 2 * k, bdk = bd + 2 * k;
+                    if (CMODE == CM_BF16) {
+                        if (CG == 2) mma_bf16_cg2(d_tmem, adk, bdk, idesc, accum);
+                        else mma_bf16(d_tmem, adk, bdk, idesc, accum);
+                    } else if (CMODE == CM_TF32) {
+                        if (CG == 2) mma_tf32_cg2(d_tmem, adk, bdk, idesc, accum);
+                        else mma_tf32(d_tmem, adk, bdk, idesc, accum);
+                    } else {
+                        if (CG == 2) {
+                            mma_tf32_cg2(d_tmem, adk + alo_off, bdk, idesc, accum);
+                            mma_tf32_cg2(d_tmem, adk, bdk + blo_off, idesc, 1u);
+                            mma_tf32_cg2(d_tmem, adk, bdk, idesc, 1u);
+                        } else {
+                            mma_tf32(d_tmem, adk + alo_off, bdk, idesc, accum);
+                            mma_tf32(d_tmem, adk, bdk + blo_off, idesc, 1u);
+                            mma_tf32(d_tmem, adk, bdk, idesc, 1u);
+                        }
+                    }
+                }
+            }
+            if (CG == 2) mma_commit_cg2(&empty[stage], 0x3);
+            else mma_commit(&empty[stage]);
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+            if (++kc == pk || kb == a.num_kb - 1) {
+                if (CG == 2) mma_commit_cg2(&tfull[acc], 0x3);
+                else mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                kc = 0;
+            }
+        }
+    }
+}
+
+// CG = CTAs per MMA: 1, or 2 (a CTA pair in a cluster issuing tcgen05.mma.cta_group::2:
+// the pair computes a 256 x BLOCK_N tile, each CTA loading its own 128 A rows and half
+// of the B rows, which halves the L2->SM operand traffic per FLOP -- the binding limit
+// of the 1-CTA kernel).
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
-                   const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1, const TcArgs a,
-                   const int tmem_cols) {
+                   const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
+                   const __grid_constant__ CUtensorMap tout, const TcArgs a, const int tmem_cols) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
-    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = a.block_n * a.row_bytes;
+    const int bn_cta = a.block_n / CG;  // B rows this CTA loads
+    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
     const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes + 8 * 32 * a.stg_row +
+                                                 (a.bias_smem ? ((a.Ncols * 4 + 15) & ~15) : 0));
     uint64_t* empty = full + a.stages;
     uint64_t* tfull = empty + a.stages;
     uint64_t* tempty = tfull + 2;
@@ -98,113 +272,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, (uint32_t)tmem_cols);
+    if (warp == 1) {
+        if (CG == 2) tmem_alloc_cg2(tmem_slot, (uint32_t)tmem_cols);
+        else tmem_alloc(tmem_slot, (uint32_t)tmem_cols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int tiles_per_batch = a.m_tiles * a.n_tiles;
     const int total_tiles = tiles_per_batch * a.batch;
     const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
+    const int unit = blockIdx.x / CG, num_units = gridDim.x / CG;  // tile scheduler works per CTA group
+    const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer
-        if (elect_one()) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-                const int b = tile / tiles_per_batch;
-                const int rem = tile % tiles_per_batch;
-                const int m0 = (rem / a.n_tiles) * BM, n0 = (rem % a.n_tiles) * a.block_n;
-                int n_img = 0, hbase = 0, wbase = 0;
-                if (a.a_mode == TC_A_IM2COL) {
-                    n_img = m0 / a.PQ;
-                    const int pq = m0 % a.PQ;
-                    hbase = (pq / a.Q) * a.sh - a.ph;
-                    wbase = (pq % a.Q) * a.sw - a.pw;
-                }
-                for (int kb = 0; kb < a.num_kb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sA = smem + stage * stage_bytes;
-                    uint8_t* sB = sA + splits * a_bytes;
-                    mbar_arrive_expect_tx(&full[stage], stage_bytes);
-                    if (a.a_mode == TC_A_IM2COL) {
-                        const int tap = kb / a.c_chunks, cc = kb % a.c_chunks;
-                        const int r = tap / a.S, s = tap % a.S;
-                        const uint16_t ow = (uint16_t)(s * a.dw), oh = (uint16_t)(r * a.dh);
-                        tma_load_im2col_4d(sA, &ta0, &full[stage], cc * kelems, wbase, hbase, n_img, ow, oh);
-                        if (splits == 2)
-                            tma_load_im2col_4d(sA + a_bytes, &ta1, &full[stage], cc * kelems, wbase, hbase, n_img, ow, oh);
-                        tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
-                        if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
-                    } else if (a.a_mode == TC_A_TILED2D) {
-                        tma_load_2d(sA, &ta0, &full[stage], kb * kelems, m0);
-                        if (splits == 2) tma_load_2d(sA + a_bytes, &ta1, &full[stage], kb * kelems, m0);
-                        tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
-                        if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
-                    } else {
-                        tma_load_3d(sA, &ta0, &full[stage], kb * kelems, m0, b);
-                        if (splits == 2) tma_load_3d(sA + a_bytes, &ta1, &full[stage], kb * kelems, m0, b);
-                        tma_load_3d(sB, &tb0, &full[stage], kb * kelems, n0, b);
-                        if (splits == 2) tma_load_3d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0, b);
-                    }
-                    if (++stage == a.stages) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
+        if (elect_one()) producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
         __syncwarp();
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        // The K loop of a tile is split into accumulation chunks of `promote_kb` K-blocks
-        // (the whole loop unless 3xTF32); each chunk goes to one of the two TMEM buffers
-        // and is handed to the epilogue, which for 3xTF32 sums the chunks in fp32
-        // registers (the tensor-core accumulator alone drifts ~7.5e-9 x K).
-        if (elect_one()) {
-            const uint32_t idesc = make_idesc(BM, a.block_n, a.cm == CM_BF16 ? 1u : 2u);
-            const int kslices = a.row_bytes / 32;
-            const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
-            int stage = 0, acc = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-                uint32_t d_tmem = 0;
-                for (int kb = 0; kb < a.num_kb; ++kb) {
-                    const int kc = kb % pk;  // position inside the accumulation chunk
-                    if (kc == 0) {
-                        mbar_wait(&tempty[acc], acc_phase ^ 1);
-                        tc_fence_after();
-                        d_tmem = tmem_base + acc * a.block_n;
-                    }
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t sA = smem_u32(smem + stage * stage_bytes);
-                    const uint32_t sB = sA + splits * a_bytes;
-                    for (int k = 0; k < kslices; ++k) {
-                        const uint32_t accumulate = (kc | k) != 0;
-                        const uint64_t ad = make_sdesc(sA + k * 32, a.row_bytes);
-                        const uint64_t bd = make_sdesc(sB + k * 32, a.row_bytes);
-                        if (a.cm == CM_BF16) {
-                            mma_bf16(d_tmem, ad, bd, idesc, accumulate);
-                        } else if (a.cm == CM_TF32) {
-                            mma_tf32(d_tmem, ad, bd, idesc, accumulate);
-                        } else {
-                            const uint64_t ad_lo = make_sdesc(sA + a_bytes + k * 32, a.row_bytes);
-                            const uint64_t bd_lo = make_sdesc(sB + b_bytes + k * 32, a.row_bytes);
-                            mma_tf32(d_tmem, ad_lo, bd, idesc, accumulate);
-                            mma_tf32(d_tmem, ad, bd_lo, idesc, 1u);
-                            mma_tf32(d_tmem, ad, bd, idesc, 1u);
-                        }
-                    }
-                    mma_commit(&empty[stage]);
-                    if (++stage == a.stages) { stage = 0; phase ^= 1; }
-                    if (kc == pk - 1 || kb == a.num_kb - 1) {
-                        mma_commit(&tfull[acc]);
-                        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                    }
-                }
+        // MMA issuer (leader CTA only); the inner loops are specialised on the operand
+        // kind and on the number of 32-byte K slices per K-block (1, 2 or 4).
+        if (leader && elect_one()) {
+            const int ks = a.row_bytes / 32;
+            if (a.cm == CM_BF16) {
+                if (ks == 4) mma_issuer<CG, CM_BF16, 4>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else if (ks == 2) mma_issuer<CG, CM_BF16, 2>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else mma_issuer<CG, CM_BF16, 1>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+            } else if (a.cm == CM_TF32) {
+                if (ks == 4) mma_issuer<CG, CM_TF32, 4>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else if (ks == 2) mma_issuer<CG, CM_TF32, 2>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else mma_issuer<CG, CM_TF32, 1>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+            } else {
+                if (ks == 4) mma_issuer<CG, CM_3XTF32, 4>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else if (ks == 2) mma_issuer<CG, CM_3XTF32, 2>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+                else mma_issuer<CG, CM_3XTF32, 1>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
             }
         }
         __syncwarp();
@@ -213,16 +318,114 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
         const int nchunks = (a.num_kb + pk - 1) / pk;
         const int ncol32 = a.block_n / 32;
+        // the MMA thread waits for all 4*CG epilogue warps of the group on the leader's barrier
+        const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+        const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0;
+        // staging buffers for TMA stores (2 per warp, 32 rows x stg_row bytes, swizzled) and bias
+        uint8_t* stg = smem + a.stages * stage_bytes;
+        float* sbias = reinterpret_cast<float*>(stg + 8 * 32 * a.stg_row);
+        uint8_t* my_stg = stg + (warp - 2) * 2 * 32 * a.stg_row;
+        if (a.bias_smem) {
+            for (int i = threadIdx.x - 64; i < a.Ncols; i += 128) sbias[i] = a.bias[i];
+            named_bar_sync(1, 128);
+        }
+        int nstore = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        auto release = [&](int which) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cluster_relaxed(which ? tempty_leader1 : tempty_leader0);
+                else mbar_arrive_relaxed(&tempty[which]);
+            }
+        };
+        // one 32-row x 32-column chunk of this warp: + bias, cast, store
+        // one 32-row x 32-column chunk of this warp: + bias, cast, store.
+        //   store_mode 0: each lane stores its own row (direct STG);
+        //   store_mode 1: stage in smem (swizzled), one TMA bulk-tensor store per chunk;
+        //   store_mode 2: stage in smem, re-read transposed so that consecutive lanes write
+        //                 consecutive 16-byte pieces of the same row (full-sector STG).
+        const uint32_t sbias_u32 = smem_u32(sbias);
+        const uint32_t stg_u32 = smem_u32(my_stg);
+        auto store_chunk = [&](float (&f)[32], int col0, int m_row0, int64_t base, int64_t cstride, bool row_ok,
+                               int b) {
+            if (a.dbg == 3) return;
+            if (a.bias) {
+                if (a.bias_smem && col0 + 32 <= a.Ncols) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 bv = lds128f(sbias_u32 + (col0 + j) * 4);
+                        f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < a.Ncols) f[j] += a.bias[col0 + j];
+                }
+            }
+            if (a.stg_row == 0 || a.store_mode == 0) {
+                if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
+                return;
+            }
+            const uint32_t buf = stg_u32 + (nstore & 1) * 32 * a.stg_row;
+            if (a.store_mode == 1 && nstore >= 2) {
+                if (lane == 0) bulk_wait_group_read<1>();
+                __syncwarp();
+            }
+            if (a.out_bf16) {  // 64-byte rows, SWIZZLE_64B: 16B chunk q of row r at q ^ ((r >> 1) & 3)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __nv_bfloat162 h[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+                    sts128(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4), *reinterpret_cast<uint4*>(h));
+                }
+            } else {  // 128-byte rows, SWIZZLE_128B: chunk q of row r at q ^ (r & 7)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 v4 = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                    sts128(buf + lane * 128 + ((q ^ (lane & 7)) << 4), *reinterpret_cast<const uint4*>(&v4));
+                }
+            }
+            if (a.store_mode == 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (a.batch > 1) tma_store_3d(&tout, my_stg + (nstore & 1) * 32 * a.stg_row, col0, m_row0, b);
+                    else tma_store_2d(&tout, my_stg + (nstore & 1) * 32 * a.stg_row, col0, m_row0);
+                    bulk_commit_group();
+                }
+            } else {
+                __syncwarp();
+                const int eo = a.out_bf16 ? 2 : 4;
+                const int per_row = a.stg_row >> 4;        // 16B pieces per row: 4 (bf16) or 8 (fp32)
+                const int rows_per_inst = 32 / per_row;    // 8 or 4
+                const int q = lane % per_row;
+                char* out = reinterpret_cast<char*>(a.out) + ((int64_t)b * a.out_bstride + col0) * eo;
+                const int valid16 = min(per_row, (a.Ncols - col0) * eo / 16);  // whole 16B pieces in range
+                const int64_t ldb = (int64_t)a.Ncols * eo;
+#pragma unroll 4
+                for (int i = 0; i < per_row; ++i) {
+                    const int r = i * rows_per_inst + lane / per_row;
+                    const int phys = a.out_bf16 ? (q ^ ((r >> 1) & 3)) : (q ^ (r & 7));
+                    const uint4 v = lds128(buf + r * a.stg_row + (phys << 4));
+                    const int mr = m_row0 + r;
+                    if (mr < a.M && q < valid16) *reinterpret_cast<uint4*>(out + (int64_t)mr * ldb + q * 16) = v;
+                }
+                __syncwarp();
+            }
+            ++nstore;
+        };
+        for (int tile = unit; tile < total_tiles; tile += num_units) {
             const int b = tile / tiles_per_batch;
             const int rem = tile % tiles_per_batch;
-            const int m0 = (rem / a.n_tiles) * BM, n0 = (rem % a.n_tiles) * a.block_n;
+            const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
+            const int n0 = (rem % a.n_tiles) * a.block_n;
             const int m = m0 + row;
+            const int m_row0 = m0 + quarter * 32;
             const bool row_ok = m < a.M;
             const int64_t ob = (int64_t)b * a.out_bstride;
             int64_t base, cstride;
@@ -237,18 +440,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (nchunks == 1) {
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
-                for (int c32 = 0; c32 < ncol32; ++c32) {
-                    uint32_t v[32];
-                    tmem_ld32(tmem_base + acc * a.block_n + c32 * 32 + lane_off, v);
+                // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
+                const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
+                uint32_t va[32], vb[32];
+                tmem_ld32(tbase, va);
+                for (int c32 = 0; c32 < ncol32; c32 += 2) {
                     tmem_ld_wait();
-                    float f[32];
+                    const bool has_b = c32 + 1 < ncol32;
+                    if (has_b) tmem_ld32(tbase + (c32 + 1) * 32, vb);
+                    else release(acc);  // TMEM drained: let the MMA reuse this buffer
+                    {
+                        float f[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-                    if (row_ok) epilogue_store(a, f, base, cstride, n0 + c32 * 32);
+                        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(va[j]);
+                        if (n0 + c32 * 32 < a.Ncols) store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b);
+                    }
+                    if (has_b) {
+                        tmem_ld_wait();
+                        const bool has_a = c32 + 2 < ncol32;
+                        if (has_a) tmem_ld32(tbase + (c32 + 2) * 32, va);
+                        else release(acc);
+                        float f[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(vb[j]);
+                        if (n0 + (c32 + 1) * 32 < a.Ncols)
+                            store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b);
+                    }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             } else {
                 // 3xTF32: sum the per-chunk tensor-core partials in fp32 registers (block_n <= 128)
@@ -270,24 +488,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             for (int j = 0; j < 32; ++j) racc[c][j] += __uint_as_float(v[j]);
                         }
                     }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    release(acc);
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
-                if (row_ok) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < ncol32) epilogue_store(a, racc[c], base, cstride, n0 + c * 32);
-                }
+                for (int c = 0; c < 4; ++c)
+                    if (c < ncol32 && n0 + c * 32 < a.Ncols)
+                        store_chunk(racc[c], n0 + c * 32, m_row0, base, cstride, row_ok, b);
             }
         }
+        if (lane == 0 && a.store_mode == 1) bulk_wait_group<0>();  // smem must outlive the last TMA stores
+        __syncwarp();
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, (uint32_t)tmem_cols);
+        if (CG == 2) tmem_dealloc_cg2(tmem_base, (uint32_t)tmem_cols);
+        else tmem_dealloc(tmem_base, (uint32_t)tmem_cols);
     }
 }
 
@@ -308,6 +526,18 @@ static int pick_block_n(int Ncols) {
     return best;
 }
 
+// CTA-group size: 2 (CTA pair, cta_group::2) unless the problem has a single 128-row
+// M tile.  AI3_TC_CG=1|2 overrides (A/B experiments).
+static int pick_cg(int M) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("AI3_TC_CG");
+        env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+    }
+    if (env) return env;
+    return M > BM ? 2 : 1;
+}
+
 void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
     if (a.block_n == 0) a.block_n = pick_block_n(a.Ncols);
@@ -315,35 +545,68 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.cm == CM_3XTF32 && a.block_n > 128) a.block_n = 128;
     // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
     a.promote_kb = a.cm == CM_3XTF32 ? (256 / (a.row_bytes / 4) > 0 ? 256 / (a.row_bytes / 4) : 1) : 0;
+    a.cg = pick_cg(a.M);
+    {
+        const char* e = getenv("AI3_TC_STORE");
+        a.store_mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+        if (a.store_mode == 0 && !a.bias_smem) a.stg_row = 0;
+    }
+    {
+        const char* e = getenv("AI3_TC_DEBUG");
+        a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
+    }
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
-    const int stage_bytes = splits * (BM + a.block_n) * a.row_bytes;
-    const int reserve = 1024 /* barriers */ + 1024 /* alignment slack */;
+    const int stage_bytes = splits * (BM + a.block_n / a.cg) * a.row_bytes;
+    if (a.bias_smem && a.Ncols > 2048) a.bias_smem = 0;
+    const int reserve = 1024 /* barriers */ + 1024 /* alignment slack */ + 8 * 32 * a.stg_row /* store staging */ +
+                        (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0);
     int stages = (SMEM_LIMIT - reserve) / stage_bytes;
     if (stages > 8) stages = 8;
     if (stages < 2) stages = 2;
     a.stages = stages;
-    a.m_tiles = (a.M + BM - 1) / BM;
+    a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
     a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
     p.smem_bytes = stages * stage_bytes + reserve;
     int cols = 32;
     while (cols < 2 * a.block_n) cols *= 2;
     p.tmem_cols = cols;
-    const long long tiles = (long long)a.m_tiles * a.n_tiles * a.batch;
-    p.grid = (int)(tiles < num_sms ? tiles : num_sms);
-    if (p.grid < 1) p.grid = 1;
+    const long long units = (long long)a.m_tiles * a.n_tiles * a.batch;  // one unit = one CTA group's tile
+    const int max_units = num_sms / a.cg;
+    p.grid = (int)(units < max_units ? units : max_units) * a.cg;
+    if (p.grid < a.cg) p.grid = a.cg;
 }
 
 cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b0,
-                      const CUtensorMap* b1, cudaStream_t st) {
+                      const CUtensorMap* b1, const CUtensorMap* out, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            SMEM_LIMIT);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    tc_gemm_kernel<<<p.grid, NUM_THREADS, p.smem_bytes, st>>>(*a0, a1 ? *a1 : *a0, *b0, b1 ? *b1 : *b0, p.args,
-                                                              p.tmem_cols);
-    return cudaGetLastError();
+    const CUtensorMap& A1 = a1 ? *a1 : *a0;
+    const CUtensorMap& B1 = b1 ? *b1 : *b0;
+    const CUtensorMap& O = out ? *out : *a0;  // unused by the kernel unless args.stg_row != 0
+    if (p.args.cg == 1) {
+        tc_gemm_kernel<1><<<p.grid, NUM_THREADS, p.smem_bytes, st>>>(*a0, A1, *b0, B1, O, p.args, p.tmem_cols);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, *a0, A1, *b0, B1, O, p.args, p.tmem_cols);
 }
 
 // ---------------------------------------------------------------- tensor-map encoding
