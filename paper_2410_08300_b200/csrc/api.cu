@@ -160,6 +160,10 @@ ai3_algo guess_rule(const ConvProblem& c) {
     if (c.G != 1) return AI3_ALGO_DIRECT;                       // only direct supports groups
     const double macs = (double)c.N * c.K * c.C * c.R * c.S * c.P * c.Q;
     if (macs < 16.0e6) return AI3_ALGO_DIRECT;                  // launch-bound: one kernel, no prep pass
+    // channels that cannot fill a 32-byte K-block row (RGB first layers, C = 3) would make the
+    // implicit GEMM pad C to 16 (bf16) / 8 (fp32) and issue one narrow MMA per filter tap;
+    // the explicit GEMM packs the exact R*S*C reduction instead
+    if (c.C * (c.dtype == AI3_BF16 ? 2 : 4) < 32) return AI3_ALGO_GEMM;
     if (check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
     g_err.clear();
     return AI3_ALGO_GEMM;
@@ -183,6 +187,7 @@ struct ai3_plan {
     ComputeMode cm = CM_BF16;
     int elem = 2, splits = 1;
     int64_t Cpad = 0;
+    int64_t Kp = 0;   // gemm: exact reduction length R*S*C padded to a 16-byte multiple
     bool need_prep = false;
     ComputeMode prep_cm = CM_BF16;
     // weight buffer regions (byte offsets into wbuf)
@@ -236,7 +241,10 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         return ok();
     }
     pl.Cpad = padded_channels(c.C, pl.elem);
-    const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad : (size_t)c.K * c.R * c.S * pl.Cpad;
+    pl.Kp = round_up(c.R * c.S * c.C, 16 / pl.elem);
+    const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad
+                          : algo == AI3_ALGO_GEMM   ? (size_t)c.K * pl.Kp
+                                                    : (size_t)c.K * c.R * c.S * pl.Cpad;
     pl.w_off = 0;
     off = align_up(wcount * e);
     pl.wlo_off = off;
@@ -250,6 +258,9 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     if (algo == AI3_ALGO_WINOGRAD) {
         pl.need_prep = !nhwc_exact;  // the input transform reads bf16 / raw fp32 and rounds itself
         pl.prep_cm = pl.cm == CM_BF16 ? CM_BF16 : CM_F32_RAW;
+    } else if (algo == AI3_ALGO_GEMM) {
+        pl.need_prep = false;  // im2col reads the raw input and writes the operand precision itself
+        pl.prep_cm = pl.cm;
     } else {
         pl.need_prep = pl.cm != CM_BF16 || !nhwc_exact;  // fp32 operands must be rounded / split
         pl.prep_cm = pl.cm;
@@ -281,7 +292,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         a.sh = c.sh; a.sw = c.sw; a.ph = c.ph; a.pw = c.pw; a.dh = c.dh; a.dw = c.dw; a.S = (int)c.S;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_GEMM) {
-        const int64_t kred = c.R * c.S * pl.Cpad;
+        const int64_t kred = pl.Kp;
         pl.ws_A = ws;
         ws = align_up(ws + (size_t)M * kred * e);
         pl.ws_Alo = ws;
@@ -290,7 +301,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         a.M = (int)M;
         a.row_bytes = tiled_row_bytes(kred * pl.elem);
         a.num_kb = (int)((kred * pl.elem + a.row_bytes - 1) / a.row_bytes);
-        pl.launches = (pl.need_prep ? 1 : 0) + pl.splits + 1;
+        pl.launches = 2;  // im2col + GEMM
     } else {  // WINOGRAD
         const int64_t T = c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2);
         pl.ws_V = ws;
@@ -335,7 +346,7 @@ ai3_status encode_b_maps(ai3_plan& pl) {
         okb = encode_tiled(&pl.tb0, dt, 3, w, dims, str, box, sw);
         if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 3, wlo, dims, str, box, sw);
     } else {
-        const uint64_t kred = (uint64_t)(c.R * c.S * pl.Cpad);
+        const uint64_t kred = pl.algo == AI3_ALGO_GEMM ? (uint64_t)pl.Kp : (uint64_t)(c.R * c.S * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
         const uint64_t str[1] = {kred * pl.elem};
         const uint32_t box[2] = {kel, (uint32_t)(a.block_n / a.cg)};
@@ -366,7 +377,7 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         oka = encode_im2col(&pl.ta0, dt, src, dims, str, lower, upper, kel, 128, es, sw);
         if (oka && pl.splits == 2) oka = encode_im2col(&pl.ta1, dt, src_lo, dims, str, lower, upper, kel, 128, es, sw);
     } else if (pl.algo == AI3_ALGO_GEMM) {
-        const uint64_t kred = (uint64_t)(c.R * c.S * pl.Cpad);
+        const uint64_t kred = (uint64_t)pl.Kp;
         const uint64_t dims[2] = {kred, (uint64_t)a.M};
         const uint64_t str[1] = {kred * e};
         const uint32_t box[2] = {kel, 128};
@@ -427,6 +438,8 @@ ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaSt
                                   reinterpret_cast<float*>(wb + pl.w_off), st);
     } else if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_filter(w, c.dtype, c.K, c.C, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
+    } else if (pl.algo == AI3_ALGO_GEMM) {
+        e = launch_pack_weights_flat(w, c.dtype, c.K, c.C, c.R, c.S, pl.Kp, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     } else {
         e = launch_pack_weights(w, c.dtype, c.K, c.C, c.R, c.S, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     }
@@ -478,11 +491,8 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = y;
     } else if (pl.algo == AI3_ALGO_GEMM) {
-        e = launch_im2col(xs, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph, c.pw, c.dh,
-                          c.dw, pl.elem, w + pl.ws_A, st);
-        if (e == cudaSuccess && pl.splits == 2)
-            e = launch_im2col(xs_lo, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph, c.pw,
-                              c.dh, c.dw, pl.elem, w + pl.ws_Alo, st);
+        e = launch_im2col(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph,
+                          c.pw, c.dh, c.dw, pl.Kp, pl.cm, w + pl.ws_A, w + pl.ws_Alo, st);
         if (e != cudaSuccess) return cuda_fail(e, "im2col launch");
         if ((s = encode_a_maps(pl, w + pl.ws_A, w + pl.ws_Alo)) != AI3_OK) return s;
         tp.args.out = y;

@@ -60,10 +60,14 @@ struct DirectArgs {
 cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- im2col / winograd transforms
-// NHWC (Cpad) -> A[M][R*S*Cpad], column order (r, s, c).
-cudaError_t launch_im2col(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P, int64_t Q,
-                          int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int elem_bytes, void* A,
-                          cudaStream_t st);
+// raw x (NCHW|NHWC, dtype) -> A[M][Kp] in compute mode (+ lo), columns (r, s, c) over the
+// exact R*S*C, zero-padded to Kp.
+cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
+                          int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t Kp,
+                          ComputeMode cm, void* A, void* A_lo, cudaStream_t st);
+// KCRS weights -> [K][Kp] with columns (r, s, c) over the exact R*S*C (zero tail), compute mode (+ lo).
+cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                     int64_t Kp, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
 // NHWC (Cpad) -> V[16][T][Cpad], T = N*ceil(P/2)*ceil(Q/2), rounded per compute mode (+ lo).
 cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P,
                                   int64_t Q, int ph, int pw, ComputeMode cm, const void* x_lo, void* V, void* V_lo,
@@ -87,6 +91,8 @@ struct TcArgs {
     int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
     int dbg;        // 0 normal; 1 = no MMA (TMA pipeline only); 2 = no TMA (MMA on stale smem); 3 = no epilogue stores -- timing probes
+    int n_acc;      // TMEM accumulator buffers (2..8)
+    int n_stg;      // epilogue smem staging buffers per warp (2, 4 or 8)
     int cg;         // CTAs per MMA group: 1 or 2 (cta_group::2 pair, 256-row tiles)
     int m_tiles, n_tiles;
     // im2col coordinates (a_mode == TC_A_IM2COL)

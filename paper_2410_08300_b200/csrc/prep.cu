@@ -103,6 +103,30 @@ cudaError_t launch_pack_weights(const void* w, ai3_dtype dtype, int64_t K, int64
     return cudaGetLastError();
 }
 
+__global__ void pack_weights_flat_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t R,
+                                         int64_t S, int64_t Kp, int cm, void* dst, void* dst_lo) {
+    const int64_t total = K * Kp;
+    const int64_t Kred = C * R * S;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / Kp, kk = i % Kp;
+        float v = 0.f;
+        if (kk < Kred) {
+            const int64_t tap = kk / C, c = kk % C;
+            const int64_t r = tap / S, s = tap % S;
+            v = load_as_f32(w, ((k * C + c) * R + r) * S + s, bf16);
+        }
+        store_cm(dst, dst_lo, i, v, cm);
+    }
+}
+
+cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                     int64_t Kp, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
+    const int64_t total = K * Kp;
+    const int grid = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+    pack_weights_flat_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, R, S, Kp, cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
 // U[xi][nu] = sum_{i,j} G[xi][i] g[i][j] G[nu][j],  G = [[1,0,0],[1/2,1/2,1/2],[1/2,-1/2,1/2],[0,0,1]]
 __global__ void winograd_filter_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t Cpad,
                                        int cm, void* dst, void* dst_lo) {

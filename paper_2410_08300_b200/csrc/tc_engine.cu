@@ -36,8 +36,10 @@ namespace ai3 {
 
 namespace {
 constexpr int BM = 128;
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_EPI_WARPS = 8;    // two epilogue warpgroups, alternating tiles
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
+constexpr int MAX_ACC = 8;          // TMEM accumulator buffers (n_acc * block_n <= 512 columns)
 }  // namespace
 
 // Store one row's 32 consecutive output channels (col0..col0+31) of a tile: + bias (fp32),
@@ -235,7 +237,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
             if (++kc == pk || kb == a.num_kb - 1) {
                 if (CG == 2) mma_commit_cg2(&tfull[acc], 0x3);
                 else mma_commit(&tfull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
                 kc = 0;
             }
         }
@@ -260,19 +262,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int bn_cta = a.block_n / CG;  // B rows this CTA loads
     const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
     const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes + 8 * 32 * a.stg_row +
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row +
                                                  (a.bias_smem ? ((a.Ncols * 4 + 15) & ~15) : 0));
     uint64_t* empty = full + a.stages;
     uint64_t* tfull = empty + a.stages;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + MAX_ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + MAX_ACC);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&ta0);
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
+        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -316,20 +318,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else {
         // ------------------------------------------------------------ epilogue (warps 2..5)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
+        const int group = (warp - 2) >> 2;  // epilogue warpgroup: takes every other tile
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const int nchunks = (a.num_kb + pk - 1) / pk;
         const int ncol32 = a.block_n / 32;
         // the MMA thread waits for all 4*CG epilogue warps of the group on the leader's barrier
-        const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
-        const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0;
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
         // staging buffers for TMA stores (2 per warp, 32 rows x stg_row bytes, swizzled) and bias
         uint8_t* stg = smem + a.stages * stage_bytes;
-        float* sbias = reinterpret_cast<float*>(stg + 8 * 32 * a.stg_row);
-        uint8_t* my_stg = stg + (warp - 2) * 2 * 32 * a.stg_row;
+        float* sbias = reinterpret_cast<float*>(stg + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row);
+        uint8_t* my_stg = stg + (warp - 2) * a.n_stg * 32 * a.stg_row;
         if (a.bias_smem) {
-            for (int i = threadIdx.x - 64; i < a.Ncols; i += 128) sbias[i] = a.bias[i];
-            named_bar_sync(1, 128);
+            for (int i = threadIdx.x - 64; i < a.Ncols; i += 32 * NUM_EPI_WARPS) sbias[i] = a.bias[i];
+            named_bar_sync(1, 32 * NUM_EPI_WARPS);
         }
         int nstore = 0;
         int acc = 0;
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (CG == 2) mbar_arrive_cluster_relaxed(which ? tempty_leader1 : tempty_leader0);
+                if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + which * 8);
                 else mbar_arrive_relaxed(&tempty[which]);
             }
         };
@@ -370,9 +372,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
                 return;
             }
-            const uint32_t buf = stg_u32 + (nstore & 1) * 32 * a.stg_row;
-            if (a.store_mode == 1 && nstore >= 2) {
-                if (lane == 0) bulk_wait_group_read<1>();
+            const int slot = nstore % a.n_stg;
+            const uint32_t buf = stg_u32 + slot * 32 * a.stg_row;
+            if (a.store_mode == 1 && nstore >= a.n_stg) {  // the store that used this slot must have read it
+                if (lane == 0) {
+                    if (a.n_stg == 8) bulk_wait_group_read<7>();
+                    else if (a.n_stg == 4) bulk_wait_group_read<3>();
+                    else bulk_wait_group_read<1>();
+                }
                 __syncwarp();
             }
             if (a.out_bf16) {  // 64-byte rows, SWIZZLE_64B: 16B chunk q of row r at q ^ ((r >> 1) & 3)
@@ -394,8 +401,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    if (a.batch > 1) tma_store_3d(&tout, my_stg + (nstore & 1) * 32 * a.stg_row, col0, m_row0, b);
-                    else tma_store_2d(&tout, my_stg + (nstore & 1) * 32 * a.stg_row, col0, m_row0);
+                    if (a.batch > 1) tma_store_3d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0, b);
+                    else tma_store_2d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0);
                     bulk_commit_group();
                 }
             } else {
@@ -419,7 +426,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             ++nstore;
         };
+        int it = -1;  // index of the tile within this CTA group's sequence
         for (int tile = unit; tile < total_tiles; tile += num_units) {
+            ++it;
+            if ((it & 1) != group) continue;
+            {
+                const int chunk0 = it * nchunks;  // accumulation chunks before this tile
+                acc = chunk0 % a.n_acc;
+                acc_phase = (uint32_t)((chunk0 / a.n_acc) & 1);
+            }
             const int b = tile / tiles_per_batch;
             const int rem = tile % tiles_per_batch;
             const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
@@ -467,19 +482,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b);
                     }
                 }
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
             } else {
-                // 3xTF32: sum the per-chunk tensor-core partials in fp32 registers (block_n <= 128)
-                float racc[4][32];
+                // 3xTF32: sum the per-chunk tensor-core partials in fp32 registers (block_n <= 64)
+                float racc[2][32];
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) racc[c][j] = 0.f;
                 for (int ch = 0; ch < nchunks; ++ch) {
                     mbar_wait(&tfull[acc], acc_phase);
                     tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < 2; ++c) {
                         if (c < ncol32) {
                             uint32_t v[32];
                             tmem_ld32(tmem_base + acc * a.block_n + c * 32 + lane_off, v);
@@ -489,10 +504,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                     }
                     release(acc);
-                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                    if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 2; ++c)
                     if (c < ncol32 && n0 + c * 32 < a.Ncols)
                         store_chunk(racc[c], n0 + c * 32, m_row0, base, cstride, row_ok, b);
             }
@@ -542,7 +557,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
     if (a.block_n == 0) a.block_n = pick_block_n(a.Ncols);
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
-    if (a.cm == CM_3XTF32 && a.block_n > 128) a.block_n = 128;
+    if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
     // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
     a.promote_kb = a.cm == CM_3XTF32 ? (256 / (a.row_bytes / 4) > 0 ? 256 / (a.row_bytes / 4) : 1) : 0;
     a.cg = pick_cg(a.M);
@@ -558,17 +573,33 @@ void tc_configure(TcPlan& p, int num_sms) {
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const int stage_bytes = splits * (BM + a.block_n / a.cg) * a.row_bytes;
     if (a.bias_smem && a.Ncols > 2048) a.bias_smem = 0;
-    const int reserve = 1024 /* barriers */ + 1024 /* alignment slack */ + 8 * 32 * a.stg_row /* store staging */ +
-                        (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0);
-    int stages = (SMEM_LIMIT - reserve) / stage_bytes;
-    if (stages > 8) stages = 8;
+    const int fixed = 1024 /* barriers */ + 1024 /* alignment slack */ + (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0);
+    // epilogue staging buffers per warp: deeper when the operand ring does not need the room
+    auto stages_for = [&](int nstg) {
+        int st = (SMEM_LIMIT - fixed - NUM_EPI_WARPS * nstg * 32 * a.stg_row) / stage_bytes;
+        return st > 8 ? 8 : st;
+    };
+    const int base_stages = stages_for(2);
+    a.n_stg = 2;
+    if (a.stg_row) {
+        for (int nstg : {4}) {
+            if (stages_for(nstg) >= base_stages) { a.n_stg = nstg; break; }
+        }
+    }
+    const int reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
+    int stages = stages_for(a.n_stg);
     if (stages < 2) stages = 2;
     a.stages = stages;
     a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
     a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
     p.smem_bytes = stages * stage_bytes + reserve;
+    // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
+    // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
+    a.n_acc = a.cm == CM_3XTF32 ? 2 : 512 / a.block_n;
+    if (a.n_acc > MAX_ACC) a.n_acc = MAX_ACC;
+    if (a.n_acc < 2) a.n_acc = 2;
     int cols = 32;
-    while (cols < 2 * a.block_n) cols *= 2;
+    while (cols < a.n_acc * a.block_n) cols *= 2;
     p.tmem_cols = cols;
     const long long units = (long long)a.m_tiles * a.n_tiles * a.batch;  // one unit = one CTA group's tile
     const int max_units = num_sms / a.cg;

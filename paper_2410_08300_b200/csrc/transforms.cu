@@ -30,34 +30,195 @@ __device__ __forceinline__ void store_v(void* dst, void* dst_lo, int64_t i, floa
 }  // namespace
 
 // ---------------------------------------------------------------- im2col
-// One thread per 16-byte vector of A.  Cpad is a multiple of the vector width.
-__global__ void im2col_kernel(const uint4* __restrict__ x, int64_t N, int64_t H, int64_t W, int64_t Cv, int64_t P,
-                              int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw,
-                              uint4* __restrict__ A) {
-    const int64_t row_v = (int64_t)R * S * Cv;  // vectors per A row
-    const int64_t total = N * P * Q * row_v;
+// A[m][kk], m = (n, p, q), kk = (r*S + s)*C + c over the exact reduction length R*S*C,
+// zero-padded to Kp (a 16-byte multiple).  Reads the caller's raw input (NCHW or NHWC,
+// fp32 or bf16) and writes the tensor-core operand precision (bf16, tf32-RN, or the
+// 3xTF32 hi/lo pair), so no separate layout pass runs.  One thread per 16-byte group of A.
+template <bool BF16IN, int V>
+__global__ void im2col_kernel(const void* __restrict__ xin, int nhwc, int64_t N, int64_t C, int64_t H, int64_t W,
+                              int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw,
+                              int64_t Kp, int cm, void* A, void* A_lo) {
+    const int64_t groups = Kp / V;
+    const int64_t Kred = (int64_t)R * S * C;
+    const int64_t total = N * P * Q * groups;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t m = i / row_v, j = i % row_v;
-        const int64_t tap = j / Cv, cv = j % Cv;
-        const int r = (int)(tap / S), s = (int)(tap % S);
+        const int64_t m = i / groups, g = i % groups;
         const int64_t n = m / (P * Q), pq = m % (P * Q);
         const int64_t p = pq / Q, q = pq % Q;
-        const int64_t ih = p * sh - ph + (int64_t)r * dh, iw = q * sw - pw + (int64_t)s * dw;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[((n * H + ih) * W + iw) * Cv + cv];
-        A[i] = v;
+        float vals[V];
+        const int64_t k0 = g * V;
+        const bool vec = nhwc && (C % V == 0) && k0 + V <= Kred;  // V channels of one tap, contiguous
+        if (vec) {
+            const int64_t tap = k0 / C, c = k0 % C;
+            const int r = (int)(tap / S), s = (int)(tap % S);
+            const int64_t ih = p * sh - ph + (int64_t)r * dh, iw = q * sw - pw + (int64_t)s * dw;
+            if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+                const int64_t off = ((n * H + ih) * W + iw) * C + c;
+                if (BF16IN) {
+                    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(xin) + off;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) vals[v] = __bfloat162float(e[v]);
+                } else {
+                    const float* e = reinterpret_cast<const float*>(xin) + off;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) vals[v] = e[v];
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) vals[v] = 0.f;
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int64_t kk = k0 + v;
+                float x = 0.f;
+                if (kk < Kred) {
+                    const int64_t tap = kk / C, c = kk % C;
+                    const int r = (int)(tap / S), s = (int)(tap % S);
+                    const int64_t ih = p * sh - ph + (int64_t)r * dh, iw = q * sw - pw + (int64_t)s * dw;
+                    if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+                        const int64_t off = nhwc ? ((n * H + ih) * W + iw) * C + c : ((n * C + c) * H + ih) * W + iw;
+                        x = BF16IN ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xin)[off])
+                                   : reinterpret_cast<const float*>(xin)[off];
+                    }
+                }
+                vals[v] = x;
+            }
+        }
+        if (cm == CM_BF16) {
+            __align__(16) __nv_bfloat16 o[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] = __float2bfloat16_rn(vals[v]);
+            reinterpret_cast<uint4*>(A)[i] = *reinterpret_cast<const uint4*>(o);
+        } else if (cm == CM_TF32) {
+            __align__(16) float o[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] = tf32_round(vals[v]);
+            reinterpret_cast<uint4*>(A)[i] = *reinterpret_cast<const uint4*>(o);
+        } else {
+            __align__(16) float hi[V], lo[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) { hi[v] = tf32_round(vals[v]); lo[v] = tf32_round(vals[v] - hi[v]); }
+            reinterpret_cast<uint4*>(A)[i] = *reinterpret_cast<const uint4*>(hi);
+            reinterpret_cast<uint4*>(A_lo)[i] = *reinterpret_cast<const uint4*>(lo);
+        }
     }
 }
 
-cudaError_t launch_im2col(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P, int64_t Q,
-                          int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int elem_bytes, void* A,
-                          cudaStream_t st) {
-    const int64_t Cv = Cpad * elem_bytes / 16;
-    const int64_t total = N * P * Q * R * S * Cv;
+// Small-C variant (RGB first layers): one CTA per (image, band of TP output rows).  The
+// band's input footprint (all W columns, all C channels) is staged once in shared memory
+// (coalesced loads, rows outside the image zeroed), then the band's A rows are written
+// with 4-8 consecutive lanes covering one row (fully coalesced 16-byte stores).
+constexpr int IM2COL_TP = 2;
+
+template <bool BF16IN, int V>
+__global__ void __launch_bounds__(256) im2col_smallc_kernel(const void* __restrict__ xin, int nhwc, int C, int H,
+                                                            int W, int P, int Q, int R, int S, int sh, int sw, int ph,
+                                                            int pw, int dh, int dw, int Kp, int FH, int cm, void* A,
+                                                            void* A_lo) {
+    extern __shared__ float band[];  // [FH][W][C]
+    const int n = blockIdx.y;
+    const int p0 = blockIdx.x * IM2COL_TP;
+    const int ih0 = p0 * sh - ph;
+    const int nb = FH * W * C;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        int y, xw, c;
+        if (nhwc) { c = i % C; const int t = i / C; xw = t % W; y = t / W; }
+        else { xw = i % W; const int t = i / W; y = t % FH; c = t / FH; }
+        const int ih = ih0 + y;
+        float v = 0.f;
+        if (ih >= 0 && ih < H) {
+            const int64_t off = nhwc ? (((int64_t)n * H + ih) * W + xw) * C + c : (((int64_t)n * C + c) * H + ih) * W + xw;
+            v = BF16IN ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xin)[off])
+                       : reinterpret_cast<const float*>(xin)[off];
+        }
+        band[(y * W + xw) * C + c] = v;
+    }
+    __syncthreads();
+    const int groups = Kp / V;
+    const int Kred = R * S * C;
+    const int rows = min(IM2COL_TP, P - p0) * Q;
+    // per-column gather table: band offset (relative to the window origin) and column shift
+    int* toff = reinterpret_cast<int*>(band + FH * W * C);
+    int* tsh = toff + Kp;
+    for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
+        if (kk < Kred) {
+            const int tap = kk / C, c = kk - tap * C;
+            const int r = tap / S, sx = tap - r * S;
+            toff[kk] = (r * dh * W + sx * dw) * C + c;
+            tsh[kk] = sx * dw;
+        } else {
+            toff[kk] = 0;
+            tsh[kk] = -(1 << 28);  // always out of range -> 0
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows * groups; i += blockDim.x) {
+        const int pix = i / groups, g = i - pix * groups;
+        const int pl = pix / Q, q = pix - pl * Q;
+        const int iw0 = q * sw - pw;
+        const int org = (pl * sh * W + iw0) * C;  // band index of the window origin (may be negative)
+        float vals[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int kk = g * V + v;
+            const int iw = iw0 + tsh[kk];
+            vals[v] = (iw >= 0 && iw < W) ? band[org + toff[kk]] : 0.f;
+        }
+        const int64_t m = ((int64_t)n * P + p0) * Q + pix;
+        const int64_t o = m * groups + g;
+        if (cm == CM_BF16) {
+            __align__(16) __nv_bfloat16 h[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) h[v] = __float2bfloat16_rn(vals[v]);
+            reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(h);
+        } else if (cm == CM_TF32) {
+            __align__(16) float h[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) h[v] = tf32_round(vals[v]);
+            reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(h);
+        } else {
+            __align__(16) float hi[V], lo[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) { hi[v] = tf32_round(vals[v]); lo[v] = tf32_round(vals[v] - hi[v]); }
+            reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(hi);
+            reinterpret_cast<uint4*>(A_lo)[o] = *reinterpret_cast<const uint4*>(lo);
+        }
+    }
+}
+
+cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
+                          int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t Kp,
+                          ComputeMode cm, void* A, void* A_lo, cudaStream_t st) {
+    {
+        const int V = cm == CM_BF16 ? 8 : 4;
+        const int FH = (IM2COL_TP - 1) * sh + (R - 1) * dh + 1;
+        const size_t smem = (size_t)FH * W * C * sizeof(float) + 2 * (size_t)Kp * sizeof(int);
+        if (C * (dtype == AI3_BF16 ? 2 : 4) < 32 && smem <= 96 * 1024 && N <= 65535) {
+            dim3 grid((unsigned)((P + IM2COL_TP - 1) / IM2COL_TP), (unsigned)N);
+            const int nhwc = in_layout == AI3_NHWC;
+            auto go = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kern<<<grid, 256, smem, st>>>(x, nhwc, (int)C, (int)H, (int)W, (int)P, (int)Q, R, S, sh, sw, ph, pw,
+                                              dh, dw, (int)Kp, FH, cm, A, A_lo);
+            };
+            if (dtype == AI3_BF16) { if (V == 8) go(im2col_smallc_kernel<true, 8>); else go(im2col_smallc_kernel<true, 4>); }
+            else { if (V == 8) go(im2col_smallc_kernel<false, 8>); else go(im2col_smallc_kernel<false, 4>); }
+            return cudaGetLastError();
+        }
+    }
+    const int V = cm == CM_BF16 ? 8 : 4;
+    const int64_t total = N * P * Q * (Kp / V);
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
-    im2col_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), N, H, W, Cv, P, Q, R, S, sh, sw, ph,
-                                        pw, dh, dw, reinterpret_cast<uint4*>(A));
+    const int nhwc = in_layout == AI3_NHWC;
+    if (dtype == AI3_BF16) {
+        if (V == 8) im2col_kernel<true, 8><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
+        else im2col_kernel<true, 4><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
+    } else {
+        if (V == 8) im2col_kernel<false, 8><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
+        else im2col_kernel<false, 4><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
+    }
     return cudaGetLastError();
 }
 
