@@ -282,7 +282,34 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     a.out_bf16 = c.dtype == AI3_BF16;
     a.out_nchw = c.out_layout == AI3_NCHW;
     a.epi_PQ = (int)(c.P * c.Q);
-    if (algo == AI3_ALGO_IMPLICIT_GEMM) {
+    // halo mode: stride-1, undilated convs with one 64-channel chunk (VGG conv1_2 / conv2_1,
+    // ResNet 64->64 3x3): one input halo per 128-pixel tile instead of R*S im2col loads
+    bool halo = false;
+    {
+        const char* e = getenv("AI3_HALO");
+        const bool allow = !(e && e[0] == '0');
+        halo = allow && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && pl.Cpad == 64 && c.sh == 1 &&
+               c.sw == 1 && c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
+               c.N <= 65535;
+    }
+    if (halo) {
+        a.a_mode = TC_A_HALO;
+        a.M = (int)M;
+        a.row_bytes = 128;
+        a.c_chunks = 1;
+        a.num_kb = 1;
+        a.Q = (int)c.Q; a.PQ = (int)(c.P * c.Q); a.P = (int)c.P;
+        a.sh = 1; a.sw = 1; a.ph = c.ph; a.pw = c.pw; a.dh = 1; a.dw = 1; a.S = (int)c.S; a.R = (int)c.R;
+        a.TP = 16; a.TQ = 8; a.RS = 16; a.HR = a.TP + (int)c.R - 1;
+        a.batch_images = (int)c.N;
+        {
+            // the tensor core applies the 128B swizzle on absolute smem address bits, so a view
+            // starting mid-atom needs no base offset (measured: base offset on -> wrong results)
+            const char* e = getenv("AI3_HALO_BO");
+            a.halo_bo = (e && e[0] == '1') ? 1 : 0;
+        }
+        pl.launches = 1 + (pl.need_prep ? 1 : 0);
+    } else if (algo == AI3_ALGO_IMPLICIT_GEMM) {
         a.a_mode = TC_A_IM2COL;
         a.M = (int)M;
         a.row_bytes = implicit_row_bytes(pl.Cpad, pl.elem);
@@ -368,7 +395,12 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
     const uint32_t kel = (uint32_t)(a.row_bytes / pl.elem);
     const uint64_t e = (uint64_t)pl.elem;
     bool oka = true;
-    if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
+    if (a.a_mode == TC_A_HALO) {
+        const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
+        const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
+        const uint32_t box[4] = {64, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+        oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
         const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
         const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
         const int lower[2] = {-c.pw, -c.ph};
@@ -408,7 +440,14 @@ ai3_status encode_out_map(ai3_plan& pl, void* out) {
     const CUtensorMapDataType dt = a.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMapSwizzle sw = a.stg_row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
     bool okm;
-    if (a.batch > 1) {
+    const ConvProblem& c = pl.pb;
+    if (a.a_mode == TC_A_HALO) {
+        const uint64_t dims[4] = {(uint64_t)a.Ncols, (uint64_t)c.Q, (uint64_t)c.P, (uint64_t)c.N};
+        const uint64_t str[3] = {(uint64_t)a.Ncols * eo, (uint64_t)c.Q * a.Ncols * eo,
+                                 (uint64_t)c.P * c.Q * a.Ncols * eo};
+        const uint32_t box[4] = {32, (uint32_t)a.TQ, (uint32_t)(32 / a.TQ), 1};
+        okm = encode_tiled(&pl.tout, dt, 4, out, dims, str, box, sw);
+    } else if (a.batch > 1) {
         const uint64_t dims[3] = {(uint64_t)a.Ncols, (uint64_t)a.M, (uint64_t)a.batch};
         const uint64_t str[2] = {(uint64_t)a.Ncols * eo, (uint64_t)a.out_bstride * eo};
         const uint32_t box[3] = {32, 32, 1};

@@ -77,7 +77,7 @@ cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, 
                                    int64_t N, int64_t K, int64_t P, int64_t Q, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 engine (tc_engine.cu)
-enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2 };
+enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2, TC_A_HALO = 3 };
 
 struct TcArgs {
     int a_mode;     // TcAMode
@@ -97,6 +97,10 @@ struct TcArgs {
     int m_tiles, n_tiles;
     // im2col coordinates (a_mode == TC_A_IM2COL)
     int Q, PQ, sh, sw, ph, pw, dh, dw, S, c_chunks;
+    // halo mode (a_mode == TC_A_HALO, stride 1, one 64-channel chunk): each CTA computes a
+    // TP x TQ output-pixel tile from one (TP+R-1) x RS-slot input halo held in smem; the
+    // R*S weight taps stay resident in smem for the whole kernel
+    int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
     // epilogue
     int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
     int out_bf16;

@@ -42,6 +42,25 @@ constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 constexpr int MAX_ACC = 8;          // TMEM accumulator buffers (n_acc * block_n <= 512 columns)
 }  // namespace
 
+
+// Shared-memory carve-up (identical on host and device):
+//   [stages x stage][resident B (halo mode)][epilogue staging][bias fp32][barriers]
+struct SmemMap {
+    uint32_t a_bytes, b_bytes, stage_bytes, bres_off, stg_off, bias_off, bar_off;
+};
+__host__ __device__ __forceinline__ SmemMap smem_map(const TcArgs& a, int cg, int num_epi_warps) {
+    SmemMap m;
+    const int splits = a.cm == CM_3XTF32 ? 2 : 1;
+    m.a_bytes = 128u * a.row_bytes;
+    m.b_bytes = (uint32_t)(a.block_n / cg) * a.row_bytes;
+    m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (m.a_bytes + m.b_bytes);
+    m.bres_off = a.stages * m.stage_bytes;
+    m.stg_off = m.bres_off + (uint32_t)a.bres_bytes;
+    m.bias_off = m.stg_off + (uint32_t)(num_epi_warps * a.n_stg * 32 * a.stg_row);
+    m.bar_off = m.bias_off + (a.bias_smem ? ((uint32_t)(a.Ncols * 4 + 15) & ~15u) : 0u);
+    return m;
+}
+
 // Store one row's 32 consecutive output channels (col0..col0+31) of a tile: + bias (fp32),
 // cast, and write NHWC-contiguous (vectorised) or NCHW (strided by P*Q; a warp's 32 rows
 // are 32 consecutive pixels, so each column store coalesces).
@@ -244,6 +263,105 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
     }
 }
 
+// ---------------------------------------------------------------- halo mode (one thread each)
+// Tile (n, tp, tq): output pixels p0..p0+TP-1 x q0..q0+TQ-1 of image n (p0 = (tp*CG + rank)*TP).
+__device__ __forceinline__ void halo_tile(const TcArgs& a, int tile, int CG, uint32_t rank, int& n, int& p0,
+                                          int& q0) {
+    const int per_img = a.tiles_p * a.tiles_q;
+    n = tile / per_img;
+    const int rem = tile - n * per_img;
+    const int tp = rem / a.tiles_q;
+    q0 = (rem - tp * a.tiles_q) * a.TQ;
+    p0 = (tp * CG + (int)rank) * a.TP;
+}
+
+template <int CG>
+__device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap& ta0, const CUtensorMap& tb0,
+                                              uint8_t* smem, uint64_t* full, uint64_t* empty, uint64_t* bres,
+                                              uint32_t rank, int unit, int num_units) {
+    const SmemMap sm = smem_map(a, CG, NUM_EPI_WARPS);
+    const int bn_cta = a.block_n / CG;
+    const int taps = a.R * a.S;
+    // resident weights: taps x bn_cta rows x 128 B (this CTA's half of the N columns)
+    uint8_t* sB = smem + sm.bres_off;
+    const int n0 = (int)rank * bn_cta;
+    if (CG == 1) {
+        mbar_arrive_expect_tx(bres, (uint32_t)a.bres_bytes);
+        for (int t = 0; t < taps; ++t) tma_load_2d(sB + t * bn_cta * 128, &tb0, bres, t * 64, n0);
+    } else {
+        if (rank == 0) mbar_arrive_expect_tx(bres, 2u * (uint32_t)a.bres_bytes);
+        const uint32_t bar = mapa_shared(smem_u32(bres), 0);
+        for (int t = 0; t < taps; ++t) tma_load_2d_cg2(sB + t * bn_cta * 128, &tb0, bar, t * 64, n0);
+    }
+    const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+    const int tiles = a.m_tiles;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = unit; tile < tiles; tile += num_units) {
+        int n, p0, q0;
+        halo_tile(a, tile, CG, rank, n, p0, q0);
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sA = smem + stage * sm.stage_bytes;
+        if (a.dbg == 2) {
+            if (rank == 0) mbar_arrive(&full[stage]);
+        } else if (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], sm.stage_bytes);
+            tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
+        } else {
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sm.stage_bytes);
+            tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
+        }
+        if (++stage == a.stages) { stage = 0; phase ^= 1; }
+    }
+}
+
+// One K-block per tile: R*S taps x 4 K slices of 16 channels.  The A view of tap (r, s)
+// starts (r*RS + s) rows into the halo; its 8-row groups (one output row of TQ = 8
+// pixels each) are RS rows apart.
+template <int CG>
+__device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                                uint64_t* tfull, uint64_t* tempty, uint64_t* bres,
+                                                uint32_t tmem_base, int unit, int num_units) {
+    const SmemMap sm = smem_map(a, CG, NUM_EPI_WARPS);
+    const int bn_cta = a.block_n / CG;
+    const uint32_t idesc = make_idesc(BM * CG, a.block_n, 1u);
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t sB = s0 + sm.bres_off;
+    const uint32_t sbo = (uint32_t)a.RS * 128u;
+    const bool no_mma = a.dbg == 1;
+    mbar_wait(bres, 0);
+    tc_fence_after();
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int tile = unit; tile < a.m_tiles; tile += num_units) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * a.block_n;
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t sA = s0 + stage * sm.stage_bytes;
+        if (!no_mma) {
+            int t = 0;
+            for (int r = 0; r < a.R; ++r) {
+                for (int sx = 0; sx < a.S; ++sx, ++t) {
+                    const uint64_t ad = make_sdesc_sw128(sA + (uint32_t)(r * a.RS + sx) * 128u, sbo, (uint32_t)a.halo_bo);
+                    const uint64_t bd = make_sdesc_sw128(sB + (uint32_t)(t * bn_cta) * 128u, 1024u, 0u);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t accum = (t > 0 || k > 0) ? 1u : 0u;
+                        if (CG == 2) mma_bf16_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                        else mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                    }
+                }
+            }
+        }
+        if (CG == 2) { mma_commit_cg2(&empty[stage], 0x3); mma_commit_cg2(&tfull[acc], 0x3); }
+        else { mma_commit(&empty[stage]); mma_commit(&tfull[acc]); }
+        if (++stage == a.stages) { stage = 0; phase ^= 1; }
+        if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
+    }
+}
+
 // CG = CTAs per MMA: 1, or 2 (a CTA pair in a cluster issuing tcgen05.mma.cta_group::2:
 // the pair computes a 256 x BLOCK_N tile, each CTA loading its own 128 A rows and half
 // of the B rows, which halves the L2->SM operand traffic per FLOP -- the binding limit
@@ -259,15 +377,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     const bool leader = rank == 0;
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
-    const int bn_cta = a.block_n / CG;  // B rows this CTA loads
-    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
-    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row +
-                                                 (a.bias_smem ? ((a.Ncols * 4 + 15) & ~15) : 0));
+    const SmemMap sm = smem_map(a, CG, NUM_EPI_WARPS);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + sm.bar_off);
     uint64_t* empty = full + a.stages;
     uint64_t* tfull = empty + a.stages;
     uint64_t* tempty = tfull + MAX_ACC;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + MAX_ACC);
+    uint64_t* bres = tempty + MAX_ACC;  // resident-B barrier (halo mode)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&ta0);
@@ -275,6 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
+        mbar_init(bres, 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -293,12 +410,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
     if (warp == 0) {
-        if (elect_one()) producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
+        if (elect_one()) {
+            if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);
+            else producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
+        }
         __syncwarp();
     } else if (warp == 1) {
         // MMA issuer (leader CTA only); the inner loops are specialised on the operand
         // kind and on the number of 32-byte K slices per K-block (1, 2 or 4).
-        if (leader && elect_one()) {
+        const bool elected = elect_one();  // one elect.sync for the whole warp
+        if (leader && elected && a.a_mode == TC_A_HALO) {
+            mma_issuer_halo<CG>(a, smem, full, empty, tfull, tempty, bres, tmem_base, unit, num_units);
+        } else if (leader && elected) {
             const int ks = a.row_bytes / 32;
             if (a.cm == CM_BF16) {
                 if (ks == 4) mma_issuer<CG, CM_BF16, 4>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
@@ -326,8 +449,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // the MMA thread waits for all 4*CG epilogue warps of the group on the leader's barrier
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
         // staging buffers for TMA stores (2 per warp, 32 rows x stg_row bytes, swizzled) and bias
-        uint8_t* stg = smem + a.stages * stage_bytes;
-        float* sbias = reinterpret_cast<float*>(stg + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row);
+        uint8_t* stg = smem + sm.stg_off;
+        float* sbias = reinterpret_cast<float*>(smem + sm.bias_off);
         uint8_t* my_stg = stg + (warp - 2) * a.n_stg * 32 * a.stg_row;
         if (a.bias_smem) {
             for (int i = threadIdx.x - 64; i < a.Ncols; i += 32 * NUM_EPI_WARPS) sbias[i] = a.bias[i];
@@ -353,7 +476,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t sbias_u32 = smem_u32(sbias);
         const uint32_t stg_u32 = smem_u32(my_stg);
         auto store_chunk = [&](float (&f)[32], int col0, int m_row0, int64_t base, int64_t cstride, bool row_ok,
-                               int b) {
+                               int b, int q0c) {
             if (a.dbg == 3) return;
             if (a.bias) {
                 if (a.bias_smem && col0 + 32 <= a.Ncols) {
@@ -401,7 +524,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    if (a.batch > 1) tma_store_3d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0, b);
+                    if (a.a_mode == TC_A_HALO) tma_store_4d(&tout, my_stg + slot * 32 * a.stg_row, col0, q0c, m_row0, b);
+                    else if (a.batch > 1) tma_store_3d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0, b);
                     else tma_store_2d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0);
                     bulk_commit_group();
                 }
@@ -435,22 +559,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 acc = chunk0 % a.n_acc;
                 acc_phase = (uint32_t)((chunk0 / a.n_acc) & 1);
             }
-            const int b = tile / tiles_per_batch;
-            const int rem = tile % tiles_per_batch;
-            const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
-            const int n0 = (rem % a.n_tiles) * a.block_n;
-            const int m = m0 + row;
-            const int m_row0 = m0 + quarter * 32;
-            const bool row_ok = m < a.M;
-            const int64_t ob = (int64_t)b * a.out_bstride;
+            int b, n0, m_row0, hn = 0, hp0 = 0, hq0 = 0;
+            bool row_ok;
             int64_t base, cstride;
-            if (a.out_nchw) {
-                const int64_t n_img = m / a.epi_PQ, pq = m % a.epi_PQ;
-                base = ob + n_img * (int64_t)a.Ncols * a.epi_PQ + pq;
-                cstride = a.epi_PQ;
+            if (a.a_mode == TC_A_HALO) {
+                // tile = TP x TQ output pixels; TMEM row = p_local * TQ + q_local
+                n0 = 0;
+                halo_tile(a, tile, CG, rank, hn, hp0, hq0);
+                b = hn;  // 4-D output store coordinate
+                const int p = hp0 + row / a.TQ, q = hq0 + row % a.TQ;
+                row_ok = p < a.P && q < a.Q;
+                m_row0 = hp0 + quarter * (32 / a.TQ);  // first output row of this warp (TMA store)
+                if (a.out_nchw) {
+                    base = ((int64_t)hn * a.Ncols) * a.PQ + (int64_t)p * a.Q + q;
+                    cstride = a.PQ;
+                } else {
+                    base = (((int64_t)hn * a.P + p) * a.Q + q) * a.Ncols;
+                    cstride = 1;
+                }
             } else {
-                base = ob + (int64_t)m * a.Ncols;
-                cstride = 1;
+                b = tile / tiles_per_batch;
+                const int rem = tile % tiles_per_batch;
+                const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
+                n0 = (rem % a.n_tiles) * a.block_n;
+                const int m = m0 + row;
+                m_row0 = m0 + quarter * 32;
+                row_ok = m < a.M;
+                const int64_t ob = (int64_t)b * a.out_bstride;
+                if (a.out_nchw) {
+                    const int64_t n_img = m / a.epi_PQ, pq = m % a.epi_PQ;
+                    base = ob + n_img * (int64_t)a.Ncols * a.epi_PQ + pq;
+                    cstride = a.epi_PQ;
+                } else {
+                    base = ob + (int64_t)m * a.Ncols;
+                    cstride = 1;
+                }
             }
             if (nchunks == 1) {
                 mbar_wait(&tfull[acc], acc_phase);
@@ -468,7 +611,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         float f[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(va[j]);
-                        if (n0 + c32 * 32 < a.Ncols) store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b);
+                        if (n0 + c32 * 32 < a.Ncols) store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b, hq0);
                     }
                     if (has_b) {
                         tmem_ld_wait();
@@ -479,7 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(vb[j]);
                         if (n0 + (c32 + 1) * 32 < a.Ncols)
-                            store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b);
+                            store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b, hq0);
                     }
                 }
                 if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
@@ -509,7 +652,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
                     if (c < ncol32 && n0 + c * 32 < a.Ncols)
-                        store_chunk(racc[c], n0 + c * 32, m_row0, base, cstride, row_ok, b);
+                        store_chunk(racc[c], n0 + c * 32, m_row0, base, cstride, row_ok, b, hq0);
             }
         }
         if (lane == 0 && a.store_mode == 1) bulk_wait_group<0>();  // smem must outlive the last TMA stores
@@ -571,9 +714,18 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
-    const int stage_bytes = splits * (BM + a.block_n / a.cg) * a.row_bytes;
+    if (a.a_mode == TC_A_HALO) {
+        // one N tile covering every output channel; weights resident per CTA
+        a.block_n = a.Ncols <= 32 ? 32 : (a.Ncols <= 64 ? 64 : 128);
+        a.halo_bytes = a.HR * a.RS * 128;
+        a.bres_bytes = a.R * a.S * (a.block_n / a.cg) * 128;
+        a.tiles_p = (a.P + a.TP * a.cg - 1) / (a.TP * a.cg);
+        a.tiles_q = (a.Q + a.TQ - 1) / a.TQ;
+    }
+    const int stage_bytes = a.a_mode == TC_A_HALO ? a.halo_bytes : splits * (BM + a.block_n / a.cg) * a.row_bytes;
     if (a.bias_smem && a.Ncols > 2048) a.bias_smem = 0;
-    const int fixed = 1024 /* barriers */ + 1024 /* alignment slack */ + (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0);
+    const int fixed = 1024 /* barriers */ + 1024 /* alignment slack */ + (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0) +
+                      a.bres_bytes;
     // epilogue staging buffers per warp: deeper when the operand ring does not need the room
     auto stages_for = [&](int nstg) {
         int st = (SMEM_LIMIT - fixed - NUM_EPI_WARPS * nstg * 32 * a.stg_row) / stage_bytes;
@@ -590,8 +742,14 @@ void tc_configure(TcPlan& p, int num_sms) {
     int stages = stages_for(a.n_stg);
     if (stages < 2) stages = 2;
     a.stages = stages;
-    a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
-    a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
+    if (a.a_mode == TC_A_HALO) {
+        a.m_tiles = a.batch_images * a.tiles_p * a.tiles_q;  // units: one (image, p-band, q-band) per CTA group
+        a.n_tiles = 1;
+        a.batch = 1;
+    } else {
+        a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
+        a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
+    }
     p.smem_bytes = stages * stage_bytes + reserve;
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
