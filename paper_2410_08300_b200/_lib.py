@@ -53,9 +53,10 @@ _lib = None
 
 def load():
     """Load libai3.so (building nothing).  Raises Ai3LibraryMissing if absent."""
-    global _lib
+    global _lib, LIB_PATH
     if _lib is not None:
         return _lib
+    LIB_PATH = os.environ.get("AI3_LIB", LIB_PATH)  # developer A/B builds; default: in-tree libai3.so
     if not os.path.exists(LIB_PATH):
         raise Ai3LibraryMissing(f"{LIB_PATH} not found: build it with `python -m paper_2410_08300_b200.build` "
                                 "(there is no CPU fallback)")

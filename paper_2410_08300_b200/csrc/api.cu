@@ -163,7 +163,15 @@ ai3_algo guess_rule(const ConvProblem& c) {
     // channels that cannot fill a 32-byte K-block row (RGB first layers, C = 3) would make the
     // implicit GEMM pad C to 16 (bf16) / 8 (fp32) and issue one narrow MMA per filter tap;
     // the explicit GEMM packs the exact R*S*C reduction instead
-    if (c.C * (c.dtype == AI3_BF16 ? 2 : 4) < 32) return AI3_ALGO_GEMM;
+    if (c.C * (c.dtype == AI3_BF16 ? 2 : 4) < 32) {
+        // ...unless the 16-byte-pixel halo mode applies (bf16, C <= 8, stride 1): it gathers
+        // all R*S taps from one smem halo per tile with no im2col round trip
+        const bool narrow_halo = c.dtype == AI3_BF16 && c.C <= 8 && c.sh == 1 && c.sw == 1 && c.dh == 1 &&
+                                 c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 && c.N <= 65535;
+        const char* e = getenv("AI3_HALO");
+        if (narrow_halo && !(e && e[0] == '0')) return AI3_ALGO_IMPLICIT_GEMM;
+        return AI3_ALGO_GEMM;
+    }
     if (check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
     g_err.clear();
     return AI3_ALGO_GEMM;
@@ -188,6 +196,8 @@ struct ai3_plan {
     int elem = 2, splits = 1;
     int64_t Cpad = 0;
     int64_t Kp = 0;   // gemm: exact reduction length R*S*C padded to a 16-byte multiple
+    int halo_pb = 0;  // implicit halo mode: bytes per halo pixel (0 = im2col TMA mode)
+    int64_t taps_pad = 0;
     bool need_prep = false;
     ComputeMode prep_cm = CM_BF16;
     // weight buffer regions (byte offsets into wbuf)
@@ -242,9 +252,22 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     }
     pl.Cpad = padded_channels(c.C, pl.elem);
     pl.Kp = round_up(c.R * c.S * c.C, 16 / pl.elem);
+    // halo modes (implicit GEMM, bf16, stride 1, undilated, K <= 128): 64 channels per pixel
+    // (128-byte swizzled rows), or <= 8 channels padded to 8 (16-byte rows, RGB first layers)
+    pl.halo_pb = 0;
+    {
+        const char* e = getenv("AI3_HALO");
+        const bool allow = !(e && e[0] == '0');
+        const bool shape_ok = algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
+                              c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
+                              c.N <= 65535;
+        if (allow && shape_ok && pl.Cpad == 64) pl.halo_pb = 128;
+        if (allow && shape_ok && c.C <= 8) { pl.halo_pb = 16; pl.Cpad = 8; }
+    }
+    pl.taps_pad = pl.halo_pb == 16 ? round_up(c.R * c.S, 2) : c.R * c.S;
     const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad
                           : algo == AI3_ALGO_GEMM   ? (size_t)c.K * pl.Kp
-                                                    : (size_t)c.K * c.R * c.S * pl.Cpad;
+                                                    : (size_t)c.K * pl.taps_pad * pl.Cpad;
     pl.w_off = 0;
     off = align_up(wcount * e);
     pl.wlo_off = off;
@@ -284,15 +307,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     a.epi_PQ = (int)(c.P * c.Q);
     // halo mode: stride-1, undilated convs with one 64-channel chunk (VGG conv1_2 / conv2_1,
     // ResNet 64->64 3x3): one input halo per 128-pixel tile instead of R*S im2col loads
-    bool halo = false;
-    {
-        const char* e = getenv("AI3_HALO");
-        const bool allow = !(e && e[0] == '0');
-        halo = allow && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && pl.Cpad == 64 && c.sh == 1 &&
-               c.sw == 1 && c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
-               c.N <= 65535;
-    }
-    if (halo) {
+    if (pl.halo_pb) {
         a.a_mode = TC_A_HALO;
         a.M = (int)M;
         a.row_bytes = 128;
@@ -301,6 +316,8 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         a.Q = (int)c.Q; a.PQ = (int)(c.P * c.Q); a.P = (int)c.P;
         a.sh = 1; a.sw = 1; a.ph = c.ph; a.pw = c.pw; a.dh = 1; a.dw = 1; a.S = (int)c.S; a.R = (int)c.R;
         a.TP = 16; a.TQ = 8; a.RS = 16; a.HR = a.TP + (int)c.R - 1;
+        a.halo_pb = pl.halo_pb;
+        a.taps_pad = (int)pl.taps_pad;
         a.batch_images = (int)c.N;
         {
             // the tensor core applies the 128B swizzle on absolute smem address bits, so a view
@@ -353,6 +370,16 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     a.stg_row = (!a.out_nchw && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
     a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
+    // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
+    {
+        const char* e = getenv("AI3_BOX64");
+        const bool allow = !(e && e[0] == '0');
+        if (allow && a.store_mode == 1 && a.stg_row == 64 && a.out_bf16 && a.block_n % 64 == 0 && a.batch == 1) {
+            a.box64 = 1;
+            a.stg_row = 128;
+            tc_configure(pl.tc, device_num_sms());  // re-derive stages / staging with 4 KB buffers
+        }
+    }
     return ok();
 }
 
@@ -372,6 +399,13 @@ ai3_status encode_b_maps(ai3_plan& pl) {
         const uint32_t box[3] = {kel, (uint32_t)(a.block_n / a.cg), 1};
         okb = encode_tiled(&pl.tb0, dt, 3, w, dims, str, box, sw);
         if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 3, wlo, dims, str, box, sw);
+    } else if (a.a_mode == TC_A_HALO) {
+        const uint64_t kred = (uint64_t)(pl.taps_pad * pl.Cpad);
+        const uint64_t dims[2] = {kred, (uint64_t)c.K};
+        const uint64_t str[1] = {kred * pl.elem};
+        const uint32_t box[2] = {(uint32_t)pl.Cpad, (uint32_t)(a.block_n / a.cg)};
+        okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box,
+                           a.halo_pb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
     } else {
         const uint64_t kred = pl.algo == AI3_ALGO_GEMM ? (uint64_t)pl.Kp : (uint64_t)(c.R * c.S * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
@@ -398,8 +432,17 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
     if (a.a_mode == TC_A_HALO) {
         const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
         const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
-        const uint32_t box[4] = {64, (uint32_t)a.RS, (uint32_t)a.HR, 1};
-        oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (a.halo_pb == 128) {
+            const uint32_t box[4] = {(uint32_t)pl.Cpad, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+            oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        } else {
+            // 16-byte pixels: view the rows as (W*Cpad, H, N) so that each halo row is one
+            // 256-byte box row (left/right padding = out-of-bounds fill on the flat axis)
+            const uint64_t d3[3] = {(uint64_t)c.W * pl.Cpad, (uint64_t)c.H, (uint64_t)c.N};
+            const uint64_t s3[2] = {c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
+            const uint32_t box[3] = {(uint32_t)(a.RS * pl.Cpad), (uint32_t)a.HR, 1};
+            oka = encode_tiled(&pl.ta0, dt, 3, src, d3, s3, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+        }
     } else if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
         const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
         const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
@@ -445,8 +488,8 @@ ai3_status encode_out_map(ai3_plan& pl, void* out) {
         const uint64_t dims[4] = {(uint64_t)a.Ncols, (uint64_t)c.Q, (uint64_t)c.P, (uint64_t)c.N};
         const uint64_t str[3] = {(uint64_t)a.Ncols * eo, (uint64_t)c.Q * a.Ncols * eo,
                                  (uint64_t)c.P * c.Q * a.Ncols * eo};
-        const uint32_t box[4] = {32, (uint32_t)a.TQ, (uint32_t)(32 / a.TQ), 1};
-        okm = encode_tiled(&pl.tout, dt, 4, out, dims, str, box, sw);
+        const uint32_t box[4] = {a.box64 ? 64u : 32u, (uint32_t)a.TQ, (uint32_t)(32 / a.TQ), 1};
+        okm = encode_tiled(&pl.tout, dt, 4, out, dims, str, box, a.box64 ? CU_TENSOR_MAP_SWIZZLE_128B : sw);
     } else if (a.batch > 1) {
         const uint64_t dims[3] = {(uint64_t)a.Ncols, (uint64_t)a.M, (uint64_t)a.batch};
         const uint64_t str[2] = {(uint64_t)a.Ncols * eo, (uint64_t)a.out_bstride * eo};
@@ -455,8 +498,8 @@ ai3_status encode_out_map(ai3_plan& pl, void* out) {
     } else {
         const uint64_t dims[2] = {(uint64_t)a.Ncols, (uint64_t)a.M};
         const uint64_t str[1] = {(uint64_t)a.Ncols * eo};
-        const uint32_t box[2] = {32, 32};
-        okm = encode_tiled(&pl.tout, dt, 2, out, dims, str, box, sw);
+        const uint32_t box[2] = {a.box64 ? 64u : 32u, 32};
+        okm = encode_tiled(&pl.tout, dt, 2, out, dims, str, box, a.box64 ? CU_TENSOR_MAP_SWIZZLE_128B : sw);
     }
     if (!okm) {
         pl.cached_out = nullptr;
@@ -477,6 +520,8 @@ ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaSt
                                   reinterpret_cast<float*>(wb + pl.w_off), st);
     } else if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_filter(w, c.dtype, c.K, c.C, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
+    } else if (pl.halo_pb) {
+        e = launch_pack_weights_taps(w, c.dtype, c.K, c.C, c.R, c.S, pl.taps_pad, pl.Cpad, pl.cm, wb + pl.w_off, st);
     } else if (pl.algo == AI3_ALGO_GEMM) {
         e = launch_pack_weights_flat(w, c.dtype, c.K, c.C, c.R, c.S, pl.Kp, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     } else {

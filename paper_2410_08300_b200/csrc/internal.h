@@ -65,6 +65,9 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st);
 cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
                           int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t Kp,
                           ComputeMode cm, void* A, void* A_lo, cudaStream_t st);
+// KCRS weights -> [K][taps_pad][Cpad] (tap = r*S + s; zero taps beyond R*S), compute mode.
+cudaError_t launch_pack_weights_taps(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                     int64_t taps_pad, int64_t Cpad, ComputeMode cm, void* dst, cudaStream_t st);
 // KCRS weights -> [K][Kp] with columns (r, s, c) over the exact R*S*C (zero tail), compute mode (+ lo).
 cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
                                      int64_t Kp, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
@@ -90,6 +93,7 @@ struct TcArgs {
     int num_kb;     // K-blocks per tile
     int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
+    int trace;      // 1: accumulate pipeline-wait cycles in g_tc_trace (AI3_TC_TRACE=1)
     int dbg;        // 0 normal; 1 = no MMA (TMA pipeline only); 2 = no TMA (MMA on stale smem); 3 = no epilogue stores -- timing probes
     int n_acc;      // TMEM accumulator buffers (2..8)
     int n_stg;      // epilogue smem staging buffers per warp (2, 4 or 8)
@@ -101,12 +105,15 @@ struct TcArgs {
     // TP x TQ output-pixel tile from one (TP+R-1) x RS-slot input halo held in smem; the
     // R*S weight taps stay resident in smem for the whole kernel
     int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
+    int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B) or 16 (<= 8 channels, no swizzle)
+    int taps_pad;   // weight taps held in smem (R*S, rounded up to even for 16-byte pixels)
     // epilogue
     int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
     int out_bf16;
     int epi_PQ;
     int stg_row;    // TMA-store epilogue: bytes per staged row (32 * out elem); 0 = direct stores
     int bias_smem;  // 1: the epilogue stages the fp32 bias in shared memory
+    int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
     const float* bias;  // fp32 [Ncols] or null
     void* out;

@@ -65,9 +65,28 @@ __global__ void prep_from_nchw_kernel(const void* __restrict__ src, int bf16, in
     }
 }
 
+// NHWC with few channels (C <= Cpad <= 8, bf16 -> bf16): one thread per pixel, one 16-byte store.
+__global__ void prep_small_nhwc_bf16_kernel(const __nv_bfloat16* __restrict__ src, int64_t pixels, int C,
+                                            uint4* __restrict__ dst) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pixels; p += (int64_t)gridDim.x * blockDim.x) {
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = c < C ? src[p * C + c] : __float2bfloat16_rn(0.f);
+        dst[p] = *reinterpret_cast<const uint4*>(v);
+    }
+}
+
 cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H,
                               int64_t W, int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
     const int bf16 = dtype == AI3_BF16;
+    if (in_layout == AI3_NHWC && bf16 && cm == CM_BF16 && Cpad == 8 && C <= 8) {
+        const int64_t pixels = N * H * W;
+        const int64_t blocks = (pixels + 255) / 256;
+        const int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
+        prep_small_nhwc_bf16_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), pixels, (int)C,
+                                                          reinterpret_cast<uint4*>(dst));
+        return cudaGetLastError();
+    }
     if (in_layout == AI3_NHWC) {
         const int64_t total = N * H * W * Cpad;
         const int64_t blocks = (total + 255) / 256;
@@ -124,6 +143,27 @@ cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, 
     const int64_t total = K * Kp;
     const int grid = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
     pack_weights_flat_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, R, S, Kp, cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
+__global__ void pack_weights_taps_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t R,
+                                         int64_t S, int64_t T, int64_t Cpad, int cm, void* dst) {
+    const int64_t total = K * T * Cpad;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % Cpad;
+        const int64_t t = (i / Cpad) % T;
+        const int64_t k = i / (Cpad * T);
+        float v = 0.f;
+        if (c < C && t < R * S) v = load_as_f32(w, ((k * C + c) * R + t / S) * S + t % S, bf16);
+        store_cm(dst, nullptr, i, v, cm);
+    }
+}
+
+cudaError_t launch_pack_weights_taps(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                     int64_t taps_pad, int64_t Cpad, ComputeMode cm, void* dst, cudaStream_t st) {
+    const int64_t total = K * taps_pad * Cpad;
+    const int grid = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+    pack_weights_taps_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, R, S, taps_pad, Cpad, cm, dst);
     return cudaGetLastError();
 }
 

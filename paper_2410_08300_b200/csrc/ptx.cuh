@@ -36,7 +36,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef AI3_MBAR_WAIT_MODE
+#define AI3_MBAR_WAIT_MODE 1
+#endif
+// mode 0: try_wait with a long suspend-time hint; 1: try_wait with the default (short)
+// hardware suspend window; 2: test_wait spin.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if AI3_MBAR_WAIT_MODE == 0
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
@@ -46,6 +52,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(0x989680u)
         : "memory");
+#elif AI3_MBAR_WAIT_MODE == 1
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA
@@ -348,5 +375,18 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t sb
     if (use_base_offset) d |= (uint64_t)((saddr >> 7) & 7u) << 49;
     d |= 2ull << 61;
     return d;
+}
+}  // namespace ai3
+
+namespace ai3 {
+// K-major SWIZZLE_NONE ("interleave") descriptor: 8-row x 16-byte core matrices, the two
+// K-adjacent core matrices of a 16-element bf16 slice `lbo` bytes apart, 8-row groups `sbo` apart.
+__device__ __forceinline__ uint64_t make_sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;
+    return d;  // layout type 0 = SWIZZLE_NONE
 }
 }  // namespace ai3

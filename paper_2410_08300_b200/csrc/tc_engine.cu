@@ -43,6 +43,25 @@ constexpr int MAX_ACC = 8;          // TMEM accumulator buffers (n_acc * block_n
 }  // namespace
 
 
+// Debug timing trace (AI3_TC_TRACE=1): per-CTA cycle counters of the pipeline waits.
+//   [0] producer: waiting for a free stage   [1] producer: total
+//   [2] MMA: waiting for operands (full)     [3] MMA: waiting for a drained accumulator
+//   [4] MMA: total                           [5] epilogue warp 2: waiting for an accumulator
+//   [6] epilogue warp 2: total               [7] tiles seen by the epilogue warp 2
+//   [8] epilogue warp 2: tcgen05.ld waits    [9] epilogue warp 2: store_chunk
+//   [10] epilogue warp 2: smem-slot waits (TMA store read)
+__device__ unsigned long long g_tc_trace[296][16];
+#define TRACE_WAIT(slot, stmt)                                                          \
+    do {                                                                                \
+        if (a.trace) {                                                                  \
+            const unsigned long long t0__ = clock64();                                  \
+            stmt;                                                                       \
+            g_tc_trace[blockIdx.x][slot] += clock64() - t0__;                           \
+        } else {                                                                        \
+            stmt;                                                                       \
+        }                                                                               \
+    } while (0)
+
 // Shared-memory carve-up (identical on host and device):
 //   [stages x stage][resident B (halo mode)][epilogue staging][bias fp32][barriers]
 struct SmemMap {
@@ -136,7 +155,7 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
         }
         int cc = 0, ts = 0, tr = 0;  // channel chunk, filter column, filter row of the current K-block
         for (int kb = 0; kb < a.num_kb; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            TRACE_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
             uint8_t* sA = smem + stage * stage_bytes;
             uint8_t* sB = sA + splits * a_bytes;
             const int kx = kb * kelems;
@@ -218,11 +237,11 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
         kc = 0;
         for (int kb = 0; kb < a.num_kb; ++kb) {
             if (kc == 0) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                TRACE_WAIT(3, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
                 d_tmem = tmem_base + acc * a.block_n;
             }
-            mbar_wait(&full[stage], phase);
+            TRACE_WAIT(2, mbar_wait(&full[stage], phase));
             tc_fence_after();
             const uint64_t soff = (uint64_t)((stage * stage_bytes) >> 4);
             const uint64_t ad = a_desc0 + soff, bd = b_desc0 + soff;
@@ -285,13 +304,15 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
     // resident weights: taps x bn_cta rows x 128 B (this CTA's half of the N columns)
     uint8_t* sB = smem + sm.bres_off;
     const int n0 = (int)rank * bn_cta;
+    const int pb = a.halo_pb, pe = pb / 2;  // bytes / bf16 elements per tap row
+    (void)taps;
     if (CG == 1) {
         mbar_arrive_expect_tx(bres, (uint32_t)a.bres_bytes);
-        for (int t = 0; t < taps; ++t) tma_load_2d(sB + t * bn_cta * 128, &tb0, bres, t * 64, n0);
+        for (int t = 0; t < a.taps_pad; ++t) tma_load_2d(sB + t * bn_cta * pb, &tb0, bres, t * pe, n0);
     } else {
         if (rank == 0) mbar_arrive_expect_tx(bres, 2u * (uint32_t)a.bres_bytes);
         const uint32_t bar = mapa_shared(smem_u32(bres), 0);
-        for (int t = 0; t < taps; ++t) tma_load_2d_cg2(sB + t * bn_cta * 128, &tb0, bar, t * 64, n0);
+        for (int t = 0; t < a.taps_pad; ++t) tma_load_2d_cg2(sB + t * bn_cta * pb, &tb0, bar, t * pe, n0);
     }
     const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
     const int tiles = a.m_tiles;
@@ -300,16 +321,22 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
     for (int tile = unit; tile < tiles; tile += num_units) {
         int n, p0, q0;
         halo_tile(a, tile, CG, rank, n, p0, q0);
-        mbar_wait(&empty[stage], phase ^ 1);
+        TRACE_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
         uint8_t* sA = smem + stage * sm.stage_bytes;
         if (a.dbg == 2) {
             if (rank == 0) mbar_arrive(&full[stage]);
         } else if (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], sm.stage_bytes);
-            tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
+            if (a.halo_pb == 16)  // (W*8, H, N) view: one 256-byte TMA row per halo row
+                tma_load_3d(sA, &ta0, &full[stage], (q0 - a.pw) * 8, p0 - a.ph, n);
+            else
+                tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
         } else {
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sm.stage_bytes);
-            tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
+            if (a.halo_pb == 16)
+                tma_load_3d_cg2(sA, &ta0, full_base + stage * 8, (q0 - a.pw) * 8, p0 - a.ph, n);
+            else
+                tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
         }
         if (++stage == a.stages) { stage = 0; phase ^= 1; }
     }
@@ -318,7 +345,7 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
 // One K-block per tile: R*S taps x 4 K slices of 16 channels.  The A view of tap (r, s)
 // starts (r*RS + s) rows into the halo; its 8-row groups (one output row of TQ = 8
 // pixels each) are RS rows apart.
-template <int CG>
+template <int CG, int R3>  // R3 = 1: compile-time 3x3 filter (descriptor offsets folded)
 __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                                 uint64_t* tfull, uint64_t* tempty, uint64_t* bres,
                                                 uint32_t tmem_base, int unit, int num_units) {
@@ -327,30 +354,81 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
     const uint32_t idesc = make_idesc(BM * CG, a.block_n, 1u);
     const uint32_t s0 = smem_u32(smem);
     const uint32_t sB = s0 + sm.bres_off;
-    const uint32_t sbo = (uint32_t)a.RS * 128u;
     const bool no_mma = a.dbg == 1;
+    const bool narrow = a.halo_pb == 16;
+    const int RSl = a.RS;  // halo row stride in pixels
+    // stage-independent descriptor parts, built once: A at halo offset 0, B per tap
+    const uint64_t a0_wide = make_sdesc_sw128(s0, (uint32_t)RSl * 128u, 0u);
+    const uint64_t b0_wide = make_sdesc_sw128(sB, 1024u, 0u);
+    const uint64_t b0_narrow = make_sdesc_none(sB, (uint32_t)bn_cta * 16u, 128u);
+    const uint32_t b_tap16 = (uint32_t)bn_cta * (narrow ? 16u : 128u) >> 4;  // B tap stride in 16-byte units
     mbar_wait(bres, 0);
     tc_fence_after();
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int tile = unit; tile < a.m_tiles; tile += num_units) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        TRACE_WAIT(3, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * a.block_n;
-        mbar_wait(&full[stage], phase);
+        TRACE_WAIT(2, mbar_wait(&full[stage], phase));
         tc_fence_after();
-        const uint32_t sA = s0 + stage * sm.stage_bytes;
-        if (!no_mma) {
-            int t = 0;
-            for (int r = 0; r < a.R; ++r) {
-                for (int sx = 0; sx < a.S; ++sx, ++t) {
-                    const uint64_t ad = make_sdesc_sw128(sA + (uint32_t)(r * a.RS + sx) * 128u, sbo, (uint32_t)a.halo_bo);
-                    const uint64_t bd = make_sdesc_sw128(sB + (uint32_t)(t * bn_cta) * 128u, 1024u, 0u);
+        const uint32_t soff16 = (stage * sm.stage_bytes) >> 4;
+        if (!no_mma && narrow) {
+            // 16-byte pixels, no swizzle: one K=16 slice = two filter taps; the second tap's
+            // core matrices sit LBO = (its halo offset - the first's) bytes further
+            const int taps = a.R * a.S;
+            const uint32_t sbo_n = (uint32_t)RSl * 16u;
+            const uint32_t sA = s0 + stage * sm.stage_bytes;
+            if (R3) {
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    const int t0 = 2 * j, t1 = 2 * j + 1;
+                    const uint32_t o0 = (uint32_t)((t0 / 3) * 16 + t0 % 3) * 16u;
+                    const uint32_t o1 = t1 < 9 ? (uint32_t)((t1 / 3) * 16 + t1 % 3) * 16u : o0 + 16u;
+                    const uint64_t ad = make_sdesc_none(sA + o0, o1 - o0, 256u);
+                    const uint64_t bd = b0_narrow + (uint64_t)(t0 * b_tap16);
+                    if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, j > 0);
+                    else mma_bf16(d_tmem, ad, bd, idesc, j > 0);
+                }
+            } else {
+                for (int j = 0; j < a.taps_pad / 2; ++j) {
+                    const int t0 = 2 * j, t1 = 2 * j + 1;
+                    const uint32_t o0 = (uint32_t)((t0 / a.S) * RSl + t0 % a.S) * 16u;
+                    const uint32_t o1 = t1 < taps ? (uint32_t)((t1 / a.S) * RSl + t1 % a.S) * 16u : o0 + 16u;
+                    const uint64_t ad = make_sdesc_none(sA + o0, o1 - o0, sbo_n);
+                    const uint64_t bd = b0_narrow + (uint64_t)(t0 * b_tap16);
+                    if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, j > 0);
+                    else mma_bf16(d_tmem, ad, bd, idesc, j > 0);
+                }
+            }
+        } else if (!no_mma) {
+            // 64-channel pixels, 128B swizzle: tap (r, s) view starts (r*RS + s) rows in; its
+            // 8-row groups are RS rows apart; 4 K slices of 32 bytes per tap
+            const uint64_t ad0 = a0_wide + soff16;
+            if (R3) {
+#pragma unroll
+                for (int t = 0; t < 9; ++t) {
+                    const uint64_t ad = ad0 + (uint64_t)(((t / 3) * 16 + t % 3) * 8);  // rows of 128 B
+                    const uint64_t bd = b0_wide + (uint64_t)(t * b_tap16);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint32_t accum = (t > 0 || k > 0) ? 1u : 0u;
                         if (CG == 2) mma_bf16_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
                         else mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                    }
+                }
+            } else {
+                int t = 0;
+                for (int r = 0; r < a.R; ++r) {
+                    for (int sx = 0; sx < a.S; ++sx, ++t) {
+                        const uint64_t ad = ad0 + (uint64_t)((r * RSl + sx) * 8);
+                        const uint64_t bd = b0_wide + (uint64_t)(t * b_tap16);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t accum = (t > 0 || k > 0) ? 1u : 0u;
+                            if (CG == 2) mma_bf16_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                            else mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                        }
                     }
                 }
             }
@@ -411,16 +489,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == 0) {
         if (elect_one()) {
-            if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);
-            else producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
+            TRACE_WAIT(1, {
+                if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);
+                else producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
+            });
         }
         __syncwarp();
     } else if (warp == 1) {
         // MMA issuer (leader CTA only); the inner loops are specialised on the operand
         // kind and on the number of 32-byte K slices per K-block (1, 2 or 4).
         const bool elected = elect_one();  // one elect.sync for the whole warp
+        const unsigned long long t_mma0 = clock64();
         if (leader && elected && a.a_mode == TC_A_HALO) {
-            mma_issuer_halo<CG>(a, smem, full, empty, tfull, tempty, bres, tmem_base, unit, num_units);
+            if (a.R == 3 && a.S == 3 && a.RS == 16)
+                mma_issuer_halo<CG, 1>(a, smem, full, empty, tfull, tempty, bres, tmem_base, unit, num_units);
+            else
+                mma_issuer_halo<CG, 0>(a, smem, full, empty, tfull, tempty, bres, tmem_base, unit, num_units);
         } else if (leader && elected) {
             const int ks = a.row_bytes / 32;
             if (a.cm == CM_BF16) {
@@ -437,8 +521,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else mma_issuer<CG, CM_3XTF32, 1>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
             }
         }
+        if (a.trace && leader && elected) g_tc_trace[blockIdx.x][4] += clock64() - t_mma0;
         __syncwarp();
     } else {
+        const unsigned long long t_epi0 = clock64();
         // ------------------------------------------------------------ epilogue (warps 2..5)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int group = (warp - 2) >> 2;  // epilogue warpgroup: takes every other tile
@@ -495,17 +581,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
                 return;
             }
+            // box64: bf16 rows of 64 channels (128 B) per TMA store -- two 32-column chunks share
+            // one staging buffer; the store leaves after the second (fewer, longer TMA rows)
+            const int half = a.box64 ? ((col0 >> 5) & 1) : 0;
             const int slot = nstore % a.n_stg;
             const uint32_t buf = stg_u32 + slot * 32 * a.stg_row;
-            if (a.store_mode == 1 && nstore >= a.n_stg) {  // the store that used this slot must have read it
+            if (a.store_mode == 1 && nstore >= a.n_stg && half == 0) {  // the store that used this slot must have read it
+                const unsigned long long tw0 = a.trace ? clock64() : 0ull;
                 if (lane == 0) {
                     if (a.n_stg == 8) bulk_wait_group_read<7>();
                     else if (a.n_stg == 4) bulk_wait_group_read<3>();
                     else bulk_wait_group_read<1>();
                 }
                 __syncwarp();
+                if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][10] += clock64() - tw0;
             }
-            if (a.out_bf16) {  // 64-byte rows, SWIZZLE_64B: 16B chunk q of row r at q ^ ((r >> 1) & 3)
+            if (a.out_bf16 && a.box64) {  // 128-byte rows, SWIZZLE_128B: piece q of row r at q ^ (r & 7)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __nv_bfloat162 h[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+                    sts128(buf + lane * 128 + (((q + 4 * half) ^ (lane & 7)) << 4), *reinterpret_cast<uint4*>(h));
+                }
+            } else if (a.out_bf16) {  // 64-byte rows, SWIZZLE_64B: 16B chunk q of row r at q ^ ((r >> 1) & 3)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     __nv_bfloat162 h[4];
@@ -521,12 +620,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             if (a.store_mode == 1) {
+                const bool last = col0 + 32 >= a.Ncols;
+                if (a.box64 && half == 0 && !last) return;  // wait for the second half of the row
                 fence_proxy_async_smem();
                 __syncwarp();
+                const int cx = col0 - 32 * half;
                 if (lane == 0) {
-                    if (a.a_mode == TC_A_HALO) tma_store_4d(&tout, my_stg + slot * 32 * a.stg_row, col0, q0c, m_row0, b);
-                    else if (a.batch > 1) tma_store_3d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0, b);
-                    else tma_store_2d(&tout, my_stg + slot * 32 * a.stg_row, col0, m_row0);
+                    if (a.a_mode == TC_A_HALO) tma_store_4d(&tout, my_stg + slot * 32 * a.stg_row, cx, q0c, m_row0, b);
+                    else if (a.batch > 1) tma_store_3d(&tout, my_stg + slot * 32 * a.stg_row, cx, m_row0, b);
+                    else tma_store_2d(&tout, my_stg + slot * 32 * a.stg_row, cx, m_row0);
                     bulk_commit_group();
                 }
             } else {
@@ -596,14 +698,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             if (nchunks == 1) {
-                mbar_wait(&tfull[acc], acc_phase);
+                if (warp == 2) { TRACE_WAIT(5, mbar_wait(&tfull[acc], acc_phase)); if (a.trace && lane == 0) g_tc_trace[blockIdx.x][7] += 1; }
+                else mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
                 const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
                 uint32_t va[32], vb[32];
                 tmem_ld32(tbase, va);
                 for (int c32 = 0; c32 < ncol32; c32 += 2) {
-                    tmem_ld_wait();
+                    if (warp == 2) TRACE_WAIT(8, tmem_ld_wait()); else tmem_ld_wait();
                     const bool has_b = c32 + 1 < ncol32;
                     if (has_b) tmem_ld32(tbase + (c32 + 1) * 32, vb);
                     else release(acc);  // TMEM drained: let the MMA reuse this buffer
@@ -611,18 +714,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         float f[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(va[j]);
-                        if (n0 + c32 * 32 < a.Ncols) store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b, hq0);
+                        if (n0 + c32 * 32 < a.Ncols) {
+                            if (warp == 2) TRACE_WAIT(9, store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b, hq0));
+                            else store_chunk(f, n0 + c32 * 32, m_row0, base, cstride, row_ok, b, hq0);
+                        }
                     }
                     if (has_b) {
-                        tmem_ld_wait();
+                        if (warp == 2) TRACE_WAIT(8, tmem_ld_wait()); else tmem_ld_wait();
                         const bool has_a = c32 + 2 < ncol32;
                         if (has_a) tmem_ld32(tbase + (c32 + 2) * 32, va);
                         else release(acc);
                         float f[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(vb[j]);
-                        if (n0 + (c32 + 1) * 32 < a.Ncols)
-                            store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b, hq0);
+                        if (n0 + (c32 + 1) * 32 < a.Ncols) {
+                            if (warp == 2) TRACE_WAIT(9, store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b, hq0));
+                            else store_chunk(f, n0 + (c32 + 1) * 32, m_row0, base, cstride, row_ok, b, hq0);
+                        }
                     }
                 }
                 if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
@@ -656,6 +764,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
         if (lane == 0 && a.store_mode == 1) bulk_wait_group<0>();  // smem must outlive the last TMA stores
+        if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][6] += clock64() - t_epi0;
         __syncwarp();
     }
     tc_fence_before();
@@ -710,6 +819,10 @@ void tc_configure(TcPlan& p, int num_sms) {
         if (a.store_mode == 0 && !a.bias_smem) a.stg_row = 0;
     }
     {
+        const char* e = getenv("AI3_TC_TRACE");
+        a.trace = (e && e[0] == '1') ? 1 : 0;
+    }
+    {
         const char* e = getenv("AI3_TC_DEBUG");
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
@@ -717,8 +830,8 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.a_mode == TC_A_HALO) {
         // one N tile covering every output channel; weights resident per CTA
         a.block_n = a.Ncols <= 32 ? 32 : (a.Ncols <= 64 ? 64 : 128);
-        a.halo_bytes = a.HR * a.RS * 128;
-        a.bres_bytes = a.R * a.S * (a.block_n / a.cg) * 128;
+        a.halo_bytes = a.HR * a.RS * a.halo_pb;
+        a.bres_bytes = a.taps_pad * (a.block_n / a.cg) * a.halo_pb;
         a.tiles_p = (a.P + a.TP * a.cg - 1) / (a.TP * a.cg);
         a.tiles_q = (a.Q + a.TQ - 1) / a.TQ;
     }
@@ -854,3 +967,12 @@ int device_num_sms() {
 }
 
 }  // namespace ai3
+
+// Debug: copy (and reset) the per-CTA pipeline-wait counters of the last traced launches.
+extern "C" int ai3_debug_tc_trace(unsigned long long* host, int rows) {
+    if (rows > 296) rows = 296;
+    if (cudaMemcpyFromSymbol(host, ai3::g_tc_trace, sizeof(unsigned long long) * 16 * rows) != cudaSuccess) return -1;
+    static unsigned long long zeros[296][16];
+    cudaMemcpyToSymbol(ai3::g_tc_trace, zeros, sizeof(zeros));
+    return rows;
+}
