@@ -93,6 +93,7 @@ struct TcArgs {
     int num_kb;     // K-blocks per tile
     int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
+    int epi_fast;   // 1: use the compile-time-specialised bf16 TMA-store epilogue when it applies
     int trace;      // 1: accumulate pipeline-wait cycles in g_tc_trace (AI3_TC_TRACE=1)
     int dbg;        // 0 normal; 1 = no MMA (TMA pipeline only); 2 = no TMA (MMA on stale smem); 3 = no epilogue stores -- timing probes
     int n_acc;      // TMEM accumulator buffers (2..8)

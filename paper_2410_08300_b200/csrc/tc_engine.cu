@@ -440,6 +440,133 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
     }
 }
 
+// ---------------------------------------------------------------- fast epilogue
+// The common case -- bf16 NHWC output through TMA stores, bias (if any) staged in smem,
+// one accumulation chunk per tile -- with every configuration choice resolved at compile
+// time, so that each 32-column chunk costs ~70 instructions (the generic path's runtime
+// branches made the epilogue instruction-bound on short-K layers).
+template <int CG, bool BOX64, bool HALO>
+__device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap& tout, uint64_t* tfull,
+                                              uint64_t* tempty, uint32_t tmem_base, uint32_t rank, int unit,
+                                              int num_units, int warp, int lane, uint8_t* my_stg, uint32_t sbias_u32) {
+    constexpr int ROWB = BOX64 ? 128 : 64;  // staging row bytes
+    const int quarter = warp & 3;
+    const int group = (warp - 2) >> 2;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int ncol32 = a.block_n / 32;
+    const int tiles_per_batch = a.m_tiles * a.n_tiles;
+    const int total_tiles = tiles_per_batch * a.batch;
+    const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+    const uint32_t stg_u32 = smem_u32(my_stg);
+    const bool has_bias = a.bias != nullptr;
+    // per-lane swizzled 16-byte slot offsets inside a staging buffer
+    uint32_t qoff[BOX64 ? 8 : 4];
+#pragma unroll
+    for (int q = 0; q < (BOX64 ? 8 : 4); ++q)
+        qoff[q] = BOX64 ? (uint32_t)(lane * 128 + ((q ^ (lane & 7)) << 4))
+                        : (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
+    int slot = 0, issued = 0;
+    const int n_stg = a.n_stg;
+    int it = -1;
+    for (int tile = unit; tile < total_tiles; tile += num_units) {
+        ++it;
+        if ((it & 1) != group) continue;
+        const int acc = it % a.n_acc;
+        const uint32_t acc_phase = (uint32_t)((it / a.n_acc) & 1);
+        int n0, row0, qc = 0, img = 0;
+        if (HALO) {
+            int hp0;
+            halo_tile(a, tile, CG, rank, img, hp0, qc);
+            n0 = 0;
+            row0 = hp0 + quarter * (32 / a.TQ);
+        } else {
+            const int rem = tile % tiles_per_batch;
+            const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
+            n0 = (rem % a.n_tiles) * a.block_n;
+            row0 = m0 + quarter * 32;
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
+        uint32_t va[32], vb[32];
+        tmem_ld32(tbase, va);
+        for (int c32 = 0; c32 < ncol32; c32 += 2) {
+            // ---- chunk c32 (even): TMEM -> regs, prefetch c32+1
+            tmem_ld_wait();
+            const bool has_b = c32 + 1 < ncol32;
+            if (has_b) tmem_ld32(tbase + (c32 + 1) * 32, vb);
+            else {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+                    else mbar_arrive_relaxed(&tempty[acc]);
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh == 1) {
+                    if (!has_b) break;
+                    tmem_ld_wait();
+                    if (c32 + 2 < ncol32) tmem_ld32(tbase + (c32 + 2) * 32, va);
+                    else {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
+                            else mbar_arrive_relaxed(&tempty[acc]);
+                        }
+                    }
+                }
+                const uint32_t* v = hh == 0 ? va : vb;
+                const int col0 = n0 + (c32 + hh) * 32;
+                if (col0 >= a.Ncols) break;
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                if (has_bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 bv = lds128f(sbias_u32 + (col0 + j) * 4);
+                        f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
+                    }
+                }
+                const int half = BOX64 ? hh : 0;
+                const uint32_t buf = stg_u32 + slot * 32 * ROWB;
+                if (half == 0 && issued >= n_stg) {  // slot reuse: that store must have read smem
+                    if (lane == 0) {
+                        if (n_stg == 4) bulk_wait_group_read<3>();
+                        else bulk_wait_group_read<1>();
+                    }
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    __nv_bfloat162 h[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+                    sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(h));
+                }
+                const bool last = col0 + 32 >= a.Ncols;
+                if (BOX64 && half == 0 && !last) continue;
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const uint8_t* src = my_stg + slot * 32 * ROWB;
+                    const int cx = col0 - 32 * half;
+                    if (HALO) tma_store_4d(&tout, src, cx, qc, row0, img);
+                    else tma_store_2d(&tout, src, cx, row0);
+                    bulk_commit_group();
+                }
+                ++issued;
+                if (++slot == n_stg) slot = 0;
+            }
+        }
+    }
+    if (lane == 0) bulk_wait_group<0>();
+    __syncwarp();
+}
+
 // CG = CTAs per MMA: 1, or 2 (a CTA pair in a cluster issuing tcgen05.mma.cta_group::2:
 // the pair computes a 256 x BLOCK_N tile, each CTA loading its own 128 A rows and half
 // of the B rows, which halves the L2->SM operand traffic per FLOP -- the binding limit
@@ -541,6 +668,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (a.bias_smem) {
             for (int i = threadIdx.x - 64; i < a.Ncols; i += 32 * NUM_EPI_WARPS) sbias[i] = a.bias[i];
             named_bar_sync(1, 32 * NUM_EPI_WARPS);
+        }
+        const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.store_mode == 1 && a.stg_row != 0 &&
+                          (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
+                          (a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
+        if (fast) {
+            const uint32_t sb = smem_u32(sbias);
+            if (a.a_mode == TC_A_HALO) {
+                if (a.box64) epilogue_fast<CG, true, true>(a, tout, tfull, tempty, tmem_base, rank, unit, num_units, warp, lane, my_stg, sb);
+                else epilogue_fast<CG, false, true>(a, tout, tfull, tempty, tmem_base, rank, unit, num_units, warp, lane, my_stg, sb);
+            } else {
+                if (a.box64) epilogue_fast<CG, true, false>(a, tout, tfull, tempty, tmem_base, rank, unit, num_units, warp, lane, my_stg, sb);
+                else epilogue_fast<CG, false, false>(a, tout, tfull, tempty, tmem_base, rank, unit, num_units, warp, lane, my_stg, sb);
+            }
         }
         int nstore = 0;
         int acc = 0;
@@ -653,7 +793,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ++nstore;
         };
         int it = -1;  // index of the tile within this CTA group's sequence
-        for (int tile = unit; tile < total_tiles; tile += num_units) {
+        for (int tile = fast ? total_tiles : unit; tile < total_tiles; tile += num_units) {
             ++it;
             if ((it & 1) != group) continue;
             {
@@ -817,6 +957,10 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_TC_STORE");
         a.store_mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
         if (a.store_mode == 0 && !a.bias_smem) a.stg_row = 0;
+    }
+    {
+        const char* e = getenv("AI3_EPI_FAST");
+        a.epi_fast = (e && e[0] == '0') ? 0 : 1;
     }
     {
         const char* e = getenv("AI3_TC_TRACE");
