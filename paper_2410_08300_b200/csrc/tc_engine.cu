@@ -536,7 +536,8 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 if (half == 0 && issued >= n_stg) {  // slot reuse: that store must have read smem
                     if (lane == 0) {
                         if (n_stg == 4) bulk_wait_group_read<3>();
-                        else bulk_wait_group_read<1>();
+                        else if (n_stg == 2) bulk_wait_group_read<1>();
+                        else bulk_wait_group_read<0>();
                     }
                     __syncwarp();
                 }
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.store_mode == 1 && a.stg_row != 0 &&
                           (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
-                          (a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
+                          (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
         if (fast) {
             const uint32_t sb = smem_u32(sbias);
             if (a.a_mode == TC_A_HALO) {
@@ -731,7 +732,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0) {
                     if (a.n_stg == 8) bulk_wait_group_read<7>();
                     else if (a.n_stg == 4) bulk_wait_group_read<3>();
-                    else bulk_wait_group_read<1>();
+                    else if (a.n_stg == 2) bulk_wait_group_read<1>();
+                    else bulk_wait_group_read<0>();
                 }
                 __syncwarp();
                 if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][10] += clock64() - tw0;
@@ -991,9 +993,8 @@ void tc_configure(TcPlan& p, int num_sms) {
     const int base_stages = stages_for(2);
     a.n_stg = 2;
     if (a.stg_row) {
-        for (int nstg : {4}) {
-            if (stages_for(nstg) >= base_stages) { a.n_stg = nstg; break; }
-        }
+        if (stages_for(4) >= base_stages) a.n_stg = 4;          // room to spare: deeper store queue
+        else if (base_stages < 6 && stages_for(1) > base_stages) a.n_stg = 1;  // long-K tiles: operand ring first
     }
     const int reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
     int stages = stages_for(a.n_stg);
