@@ -923,13 +923,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // N tile: minimise n_tiles * max(BLOCK_N, 96) -- below ~96 columns an MMA is bound by
 // re-reading the 128-row A tile from shared memory, not by the tensor pipe.  Ties go to
 // the smaller tile (less padding, more CTAs).
-static int pick_block_n(int Ncols) {
+static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups) {
+    // time ~ waves x per-tile cost; per-tile cost ~ max(BLOCK_N, 96) (MMA) + 48 (A-tile load and
+    // epilogue overheads that do not shrink with BLOCK_N).  Partial last waves count in full.
     const int cands[4] = {32, 64, 128, 256};
     int best = 32;
     long long best_cost = -1;
     for (int bn : cands) {
-        const long long tiles = (Ncols + bn - 1) / bn;
-        const long long cost = tiles * (bn > 96 ? bn : 96);
+        const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
+        const long long waves = (units + num_groups - 1) / num_groups;
+        const long long cost = waves * ((bn > 96 ? bn : 96) + 48);
         if (best_cost < 0 || cost < best_cost) { best = bn; best_cost = cost; }
     }
     return best;
@@ -949,7 +952,15 @@ static int pick_cg(int M) {
 
 void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
-    if (a.block_n == 0) a.block_n = pick_block_n(a.Ncols);
+    if (a.block_n == 0 && a.a_mode != TC_A_HALO) {
+        const char* e = getenv("AI3_BN");  // experiment override: force BLOCK_N
+        if (e && atoi(e) > 0) a.block_n = atoi(e);
+    }
+    if (a.block_n == 0) {
+        const int cg = pick_cg(a.M);
+        const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
+        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg);
+    }
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
     if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
     // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
