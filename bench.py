@@ -296,14 +296,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     per_algo = None
     if not args.no_compare and rank == 0:
         per_algo = {}
-        for algo in ("implicit_gemm", "winograd", "gemm", "direct"):
+        for algo in ("implicit_gemm", "winograd", "gemm", "kn2row", "direct", "smm"):
             if algo == args.algo:
                 per_algo[algo] = round(value / world, 1)
                 continue
             try:
                 alt = [Layer(s, algo, device, seed=1000 * 2 + i) for i, s in enumerate(specs)]
                 _time_stack(alt, 1, stream, per_layer=False)
-                reps = 3 if algo != "direct" else 1
+                reps = 3 if algo not in ("direct", "smm") else 1
                 ms, _ = _time_stack(alt, reps, stream, per_layer=False)
                 per_algo[algo] = round(step_flops / (ms / reps * 1e-3) / 1e12, 1)
                 del alt

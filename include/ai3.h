@@ -71,11 +71,11 @@ typedef enum {
     AI3_ALGO_GEMM = 2,              /* "gemm", "im2col" */
     AI3_ALGO_IMPLICIT_GEMM = 3,     /* "implicit_gemm" */
     AI3_ALGO_WINOGRAD = 4,          /* "winograd" */
-    /* reserved names, recognised but AI3_ERR_UNSUPPORTED until built */
+    /* SURVEY §8f rows; "implicit_precomp_gemm" is AI3_ERR_UNSUPPORTED until built */
     AI3_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* "implicit_precomp_gemm" */
-    AI3_ALGO_SMM = 6,               /* "smm" */
-    AI3_ALGO_KN2ROW = 7,            /* "kn2row" */
-    AI3_ALGO_CUSTOM = 8             /* "custom" */
+    AI3_ALGO_SMM = 6,               /* "smm": scalar matrix multiplication (§II.B(c)) */
+    AI3_ALGO_KN2ROW = 7,            /* "kn2row": kernel-to-row 1x1 GEMMs + shift-accumulate (§II.B(b)) */
+    AI3_ALGO_CUSTOM = 8             /* "custom": the registered user algorithm (see below) */
 } ai3_algo;
 
 typedef enum { AI3_F32 = 0, AI3_BF16 = 1 } ai3_dtype;
@@ -202,6 +202,53 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
 
 /* Free the plan's host-side state (never the caller's device buffers). NULL is a no-op. */
 void ai3_conv2d_plan_destroy(ai3_plan* plan);
+
+/* ------------------------------------------------------------------ custom algorithms
+ *
+ * users implement their own convolution and select it "in the same
+ * manner the built-in implementations are" (:80) -- by its name, by "custom", or through
+ * "default" when registered as the default (:170; the paper's per-operation header
+ * boolean).  Registration is at run time here.
+ *
+ * A custom function receives exactly the operands of ai3_conv2d (x, KCRS w, bias or NULL,
+ * stride/padding/dilation pairs, groups, caller-allocated y, the stream) plus the
+ * user_data pointer given at registration; it must enqueue its work on `stream` and
+ * return AI3_OK or an error status.  ai3 does not check what it computes. */
+typedef ai3_status (*ai3_conv2d_custom_fn)(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias,
+                                           const int32_t stride[2], const int32_t padding[2],
+                                           const int32_t dilation[2], int32_t groups, ai3_tensor4d* y,
+                                           void* stream, void* user_data);
+
+/* Register `fn` under `name` (copied).  Errors: AI3_ERR_INVALID_ARGUMENT for a null/empty
+ * name or fn, a built-in algorithm name or selection keyword ("custom", "default",
+ * "torch", "keep", "guess", "auto", "benchmark", ...), or use_as_default while another
+ * name is the default.  Re-registering a name replaces its entry.  Thread-safe. */
+ai3_status ai3_register_conv2d(const char* name, ai3_conv2d_custom_fn fn, void* user_data,
+                               int32_t use_as_default);
+
+/* Remove a registered algorithm (AI3_ERR_UNKNOWN_ALGORITHM if not registered). */
+ai3_status ai3_unregister_conv2d(const char* name);
+
+/* Number of registered custom conv2d algorithms. */
+int32_t ai3_custom_conv2d_count(void);
+
+/* Resolve a selector name:
+ *   "custom"          -> the unique registered algorithm (AI3_ERR_UNKNOWN_ALGORITHM if none,
+ *                        AI3_ERR_INVALID_ARGUMENT if several: select one by name);
+ *   "default"         -> the algorithm registered with use_as_default, else AI3_ALGO_GUESS;
+ *   a registered name -> that algorithm;
+ *   a built-in name   -> its ai3_algo.
+ * Custom resolutions set *algo = AI3_ALGO_CUSTOM and copy the resolved name into
+ * custom_name (cap bytes, NUL-terminated; may be NULL); otherwise custom_name = "". */
+ai3_status ai3_conv2d_resolve(const char* name, ai3_algo* algo, char* custom_name, size_t cap);
+
+/* Run the custom algorithm `name` ("custom", "default" or a registered name) on the
+ * ai3_conv2d operands.  Returns the function's status, or AI3_ERR_UNKNOWN_ALGORITHM if
+ * `name` resolves to no registered algorithm.  ai3_conv2d with AI3_ALGO_CUSTOM is
+ * ai3_conv2d_custom("custom", ...).  Custom algorithms have no plans. */
+ai3_status ai3_conv2d_custom(const char* name, const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias,
+                             const int32_t stride[2], const int32_t padding[2], const int32_t dilation[2],
+                             int32_t groups, ai3_tensor4d* y, void* stream);
 
 #ifdef __cplusplus
 }

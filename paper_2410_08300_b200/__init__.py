@@ -6,18 +6,23 @@
     m = ai3.swap_backend(model, {"conv2d": selector})        # traced model
 
 Algorithms (PAPER.md:53-56, :192-195, :200): "direct", "gemm" (= "im2col"),
-"implicit_gemm", "winograd", and "guess" (= "default" = "auto").  All run as
+"implicit_gemm", "winograd", "smm", "kn2row", and "guess" (= "auto"; "default" is
+the registered default custom algorithm if any, else "guess").
+User algorithms: ``register_conv2d(name, fn, use_as_default)``, selected by name or
+"custom".  All run as
 sm_100a kernels in libai3.so behind the C ABI in include/ai3.h; PyTorch only
 provides device memory, streams and the module objects.
 """
 from ._lib import Ai3LibraryMissing, LIB_PATH
 from .conv import (ALGORITHMS, Ai3Error, ConvPlan, UnknownAlgorithm, UnsupportedConfiguration, algo_id, algo_name,
                    check_supported, conv2d, guess, output_shape, supported)
+from .custom import register_conv2d, registered_count, unregister_conv2d
 from .hooks import Conv2D, Model, swap_backend, swap_conv2d
 
 __all__ = ["ALGORITHMS", "Ai3Error", "Ai3LibraryMissing", "Conv2D", "ConvPlan", "LIB_PATH", "Model",
            "UnknownAlgorithm", "UnsupportedConfiguration", "algo_id", "algo_name", "check_supported", "conv2d",
-           "guess", "output_shape", "supported", "swap_backend", "swap_conv2d", "version"]
+           "guess", "output_shape", "register_conv2d", "registered_count", "supported", "swap_backend", "swap_conv2d",
+           "unregister_conv2d", "version"]
 
 
 def version() -> int:

@@ -30,7 +30,8 @@ EXPORTS = ["ai3_version", "ai3_last_error", "ai3_algo_name", "ai3_algo_from_name
            "ai3_conv2d_supported", "ai3_conv2d_guess", "ai3_conv2d_workspace_size", "ai3_conv2d",
            "ai3_conv2d_plan_weight_bytes", "ai3_conv2d_plan_create", "ai3_conv2d_plan_algo",
            "ai3_conv2d_plan_workspace_size", "ai3_conv2d_plan_num_launches", "ai3_conv2d_plan_execute",
-           "ai3_conv2d_plan_execute_host", "ai3_conv2d_plan_destroy"]
+           "ai3_conv2d_plan_execute_host", "ai3_conv2d_plan_destroy", "ai3_register_conv2d",
+           "ai3_unregister_conv2d", "ai3_custom_conv2d_count", "ai3_conv2d_resolve", "ai3_conv2d_custom"]
 
 
 class Ai3LibraryMissing(RuntimeError):
@@ -47,6 +48,12 @@ class Tensor4d(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("n", ctypes.c_int64), ("c", ctypes.c_int64), ("h", ctypes.c_int64),
                 ("w", ctypes.c_int64), ("dtype", ctypes.c_int32), ("layout", ctypes.c_int32)]
 
+
+# ai3_conv2d_custom_fn (include/ai3.h)
+CUSTOM_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), ctypes.c_void_p,
+                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                             ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.POINTER(Tensor4d),
+                             ctypes.c_void_p, ctypes.c_void_p)
 
 _lib = None
 
@@ -87,6 +94,12 @@ def load():
         "ai3_conv2d_plan_execute": ([vp, vp, vp, vp, sz, vp], ctypes.c_int),
         "ai3_conv2d_plan_execute_host": ([vp, vp, vp, vp, vp, vp, sz, vp], ctypes.c_int),
         "ai3_conv2d_plan_destroy": ([vp], None),
+        "ai3_register_conv2d": ([ctypes.c_char_p, vp, vp, i32], ctypes.c_int),
+        "ai3_unregister_conv2d": ([ctypes.c_char_p], ctypes.c_int),
+        "ai3_custom_conv2d_count": ([], i32),
+        "ai3_conv2d_resolve": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, sz], ctypes.c_int),
+        "ai3_conv2d_custom": ([ctypes.c_char_p, ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), vp, i32x2, i32x2,
+                               i32x2, i32, ctypes.POINTER(Tensor4d), vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

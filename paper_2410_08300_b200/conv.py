@@ -13,8 +13,8 @@ import torch
 
 from . import _lib
 
-ALGORITHMS = ("guess", "default", "auto", "direct", "gemm", "im2col", "implicit_gemm", "winograd",
-              "implicit_precomp_gemm", "smm", "kn2row", "custom")
+ALGORITHMS = ("guess", "default", "auto", "direct", "gemm", "im2col", "implicit_gemm", "winograd", "smm", "kn2row",
+              "implicit_precomp_gemm", "custom")
 
 
 class Ai3Error(RuntimeError):
@@ -49,6 +49,19 @@ def algo_id(name) -> int:
     if st != _lib.OK:
         raise UnknownAlgorithm(_lib.last_error())
     return out.value
+
+
+def resolve(name) -> tuple[int, str | None]:
+    """Selector name -> (ai3_algo id, registered custom name or None) via ai3_conv2d_resolve
+    ("custom", "default" -> a registered default first, registered names)."""
+    if isinstance(name, int):
+        return name, None
+    out = ctypes.c_int()
+    buf = ctypes.create_string_buffer(256)
+    st = _lib.load().ai3_conv2d_resolve(str(name).encode(), ctypes.byref(out), buf, 256)
+    if st != _lib.OK:
+        _check(st)
+    return out.value, (buf.value.decode() if out.value == _lib.ALGO_CUSTOM else None)
 
 
 def algo_name(aid: int) -> str:
@@ -187,14 +200,26 @@ def conv2d(input: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None 
     if out is None:
         out = torch.empty(oshape, dtype=input.dtype, device=input.device, memory_format=fmt)
     out_layout = layout_of(out)
+    arr = lambda v: (ctypes.c_int32 * 2)(*v)  # noqa: E731
+    aid, custom = resolve(algorithm)
+    if aid == _lib.ALGO_CUSTOM and custom is None:
+        custom = "custom"
+    if custom is not None:  # a registered user algorithm, dispatched by libai3's registry
+        xd, wd, yd = _desc(input, in_layout), _desc(weight, _lib.NCHW), _desc(out, out_layout)
+        with torch.cuda.device(input.device):
+            st = lib.ai3_conv2d_custom(custom.encode(), ctypes.byref(xd), ctypes.byref(wd),
+                                       None if bias is None else bias.data_ptr(), arr(s), arr(p), arr(d),
+                                       int(groups), ctypes.byref(yd), _stream_ptr(input.device))
+        if st != _lib.OK:
+            from .custom import last_python_error
+            raise Ai3Error(st, f"custom conv2d '{custom}' failed: {_lib.last_error() or last_python_error()}")
+        return out
     prm = _lib.params(weight.shape[0], weight.shape[2:], s, p, d, groups, bias is not None)
-    aid = algo_id(algorithm)
     nbytes = ctypes.c_size_t()
     _check(lib.ai3_conv2d_workspace_size(ctypes.byref(prm), _lib.shape4(input.shape), _dtype_id(input.dtype),
                                          _math_id(math), aid, in_layout, out_layout, ctypes.byref(nbytes)))
     ws = _WS.get(input.device, nbytes.value)
     xd, wd, yd = _desc(input, in_layout), _desc(weight, _lib.NCHW), _desc(out, out_layout)
-    arr = lambda v: (ctypes.c_int32 * 2)(*v)  # noqa: E731
     with torch.cuda.device(input.device):
         st = lib.ai3_conv2d(ctypes.byref(xd), ctypes.byref(wd), None if bias is None else bias.data_ptr(),
                             arr(s), arr(p), arr(d), int(groups), aid, _math_id(math), ctypes.byref(yd),

@@ -145,10 +145,20 @@ ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
             if (c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2) >= (1LL << 31))
                 return fail(AI3_ERR_UNSUPPORTED, "winograd: tile count >= 2^31");
             return ok();
-        case AI3_ALGO_IMPLICIT_PRECOMP_GEMM:
         case AI3_ALGO_SMM:
+            if (c.N * c.G > 65535) return fail(AI3_ERR_UNSUPPORTED, "smm: N*groups > 65535");
+            return ok();
         case AI3_ALGO_KN2ROW:
+            if (c.G != 1) return fail(AI3_ERR_UNSUPPORTED, "kn2row requires groups == 1 (got %d); use direct or smm", c.G);
+            if (c.N * c.H * c.W >= (1LL << 31) || c.R * c.S * c.K >= (1LL << 31))
+                return fail(AI3_ERR_UNSUPPORTED, "kn2row: N*H*W or R*S*K >= 2^31");
+            return ok();
         case AI3_ALGO_CUSTOM:
+            // what a user algorithm supports is its own business (e.g. grouped conv)
+            if (ai3_custom_conv2d_count() == 0)
+                return fail(AI3_ERR_UNSUPPORTED, "'custom' selected but no custom conv2d algorithm is registered");
+            return ok();
+        case AI3_ALGO_IMPLICIT_PRECOMP_GEMM:
             return fail(AI3_ERR_UNSUPPORTED, "algorithm '%s' is reserved and not built yet", ai3_algo_name(algo));
     }
     return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
@@ -187,6 +197,8 @@ ai3_status resolve_algo(const ConvProblem& c, ai3_algo algo, ai3_algo* out) {
 }
 
 }  // namespace
+
+ai3_status ai3::api_fail(ai3_status st, const char* msg) { return fail(st, "%s", msg); }
 
 // ---------------------------------------------------------------- the plan
 struct ai3_plan {
@@ -230,6 +242,8 @@ CUtensorMapSwizzle map_swizzle(int row_bytes) {
 
 // Fill sizes / offsets of a plan (no device work).  algo must be resolved.
 ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
+    if (algo == AI3_ALGO_CUSTOM)
+        return fail(AI3_ERR_UNSUPPORTED, "custom algorithms have no plans: run them with ai3_conv2d / ai3_conv2d_custom");
     pl.pb = c;
     pl.algo = algo;
     pl.cm = compute_mode(c);
@@ -238,7 +252,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     pl.bias_present = c.has_bias;
     const size_t e = (size_t)pl.elem;
     size_t off = 0;
-    if (algo == AI3_ALGO_DIRECT) {
+    if (algo == AI3_ALGO_DIRECT || algo == AI3_ALGO_SMM) {
         const int64_t Kg = c.K / c.G, Cg = c.C / c.G;
         pl.Kgp = round_up(Kg, 32);
         pl.w_off = 0;
@@ -251,7 +265,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         return ok();
     }
     pl.Cpad = padded_channels(c.C, pl.elem);
-    pl.Kp = round_up(c.R * c.S * c.C, 16 / pl.elem);
+    pl.Kp = algo == AI3_ALGO_KN2ROW ? pl.Cpad : round_up(c.R * c.S * c.C, 16 / pl.elem);
     // halo modes (implicit GEMM, bf16, stride 1, undilated, K <= 128): 64 channels per pixel
     // (128-byte swizzled rows), or <= 8 channels padded to 8 (16-byte rows, RGB first layers)
     pl.halo_pb = 0;
@@ -267,6 +281,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     pl.taps_pad = pl.halo_pb == 16 ? round_up(c.R * c.S, 2) : c.R * c.S;
     const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad
                           : algo == AI3_ALGO_GEMM   ? (size_t)c.K * pl.Kp
+                          : algo == AI3_ALGO_KN2ROW ? (size_t)c.R * c.S * c.K * pl.Cpad
                                                     : (size_t)c.K * pl.taps_pad * pl.Cpad;
     pl.w_off = 0;
     off = align_up(wcount * e);
@@ -346,6 +361,19 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         a.row_bytes = tiled_row_bytes(kred * pl.elem);
         a.num_kb = (int)((kred * pl.elem + a.row_bytes - 1) / a.row_bytes);
         pl.launches = 2;  // im2col + GEMM
+    } else if (algo == AI3_ALGO_KN2ROW) {
+        // one GEMM over every input pixel: Z[N*H*W][R*S*K] (fp32 partial planes), then shift-accumulate
+        const int64_t Mz = c.N * c.H * c.W;
+        pl.ws_M = ws;
+        ws = align_up(ws + (size_t)Mz * c.R * c.S * c.K * 4);
+        a.a_mode = TC_A_TILED2D;
+        a.M = (int)Mz;
+        a.Ncols = (int)(c.R * c.S * c.K);
+        a.row_bytes = tiled_row_bytes(pl.Cpad * pl.elem);
+        a.num_kb = (int)((pl.Cpad * pl.elem + a.row_bytes - 1) / a.row_bytes);
+        a.out_bf16 = 0;
+        a.out_nchw = 0;
+        pl.launches = (pl.need_prep ? 1 : 0) + 2;
     } else {  // WINOGRAD
         const int64_t T = c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2);
         pl.ws_V = ws;
@@ -368,7 +396,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     // TMA-store epilogue for row-major (NHWC / [b][T][K]) outputs whose rows are 16-byte multiples
     const int eo = a.out_bf16 ? 2 : 4;
     a.stg_row = (!a.out_nchw && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
-    a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD) ? 1 : 0;
+    a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD && algo != AI3_ALGO_KN2ROW) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
     {
@@ -399,6 +427,12 @@ ai3_status encode_b_maps(ai3_plan& pl) {
         const uint32_t box[3] = {kel, (uint32_t)(a.block_n / a.cg), 1};
         okb = encode_tiled(&pl.tb0, dt, 3, w, dims, str, box, sw);
         if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 3, wlo, dims, str, box, sw);
+    } else if (pl.algo == AI3_ALGO_KN2ROW) {
+        const uint64_t dims[2] = {(uint64_t)pl.Cpad, (uint64_t)(c.R * c.S * c.K)};
+        const uint64_t str[1] = {(uint64_t)pl.Cpad * pl.elem};
+        const uint32_t box[2] = {kel, (uint32_t)(a.block_n / a.cg)};
+        okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box, sw);
+        if (okb && pl.splits == 2) okb = encode_tiled(&pl.tb1, dt, 2, wlo, dims, str, box, sw);
     } else if (a.a_mode == TC_A_HALO) {
         const uint64_t kred = (uint64_t)(pl.taps_pad * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
@@ -451,7 +485,7 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         const uint32_t es[4] = {1, (uint32_t)c.sw, (uint32_t)c.sh, 1};
         oka = encode_im2col(&pl.ta0, dt, src, dims, str, lower, upper, kel, 128, es, sw);
         if (oka && pl.splits == 2) oka = encode_im2col(&pl.ta1, dt, src_lo, dims, str, lower, upper, kel, 128, es, sw);
-    } else if (pl.algo == AI3_ALGO_GEMM) {
+    } else if (pl.algo == AI3_ALGO_GEMM || pl.algo == AI3_ALGO_KN2ROW) {
         const uint64_t kred = (uint64_t)pl.Kp;
         const uint64_t dims[2] = {kred, (uint64_t)a.M};
         const uint64_t str[1] = {kred * e};
@@ -515,13 +549,16 @@ ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaSt
     const ConvProblem& c = pl.pb;
     cudaError_t e = cudaSuccess;
     char* wb = pl.wbuf;
-    if (pl.algo == AI3_ALGO_DIRECT) {
+    if (pl.algo == AI3_ALGO_DIRECT || pl.algo == AI3_ALGO_SMM) {
         e = launch_direct_weights(w, c.dtype, c.K, c.C / c.G, c.R, c.S, c.G, pl.Kgp,
                                   reinterpret_cast<float*>(wb + pl.w_off), st);
     } else if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_filter(w, c.dtype, c.K, c.C, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     } else if (pl.halo_pb) {
         e = launch_pack_weights_taps(w, c.dtype, c.K, c.C, c.R, c.S, pl.taps_pad, pl.Cpad, pl.cm, wb + pl.w_off, st);
+    } else if (pl.algo == AI3_ALGO_KN2ROW) {
+        e = launch_pack_weights_kn2row(w, c.dtype, c.K, c.C, c.R, c.S, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off,
+                                       st);
     } else if (pl.algo == AI3_ALGO_GEMM) {
         e = launch_pack_weights_flat(w, c.dtype, c.K, c.C, c.R, c.S, pl.Kp, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     } else {
@@ -544,15 +581,15 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     const float* bias = pl.bias_present ? reinterpret_cast<const float*>(pl.wbuf + pl.bias_off) : nullptr;
     char* w = reinterpret_cast<char*>(ws);
     cudaError_t e = cudaSuccess;
-    if (pl.algo == AI3_ALGO_DIRECT) {
+    if (pl.algo == AI3_ALGO_DIRECT || pl.algo == AI3_ALGO_SMM) {
         DirectArgs d{};
         d.x = x; d.w = reinterpret_cast<const float*>(pl.wbuf + pl.w_off); d.bias = bias; d.y = y;
         d.N = c.N; d.C = c.C; d.H = c.H; d.W = c.W; d.K = c.K; d.P = c.P; d.Q = c.Q;
         d.R = (int)c.R; d.S = (int)c.S; d.sh = c.sh; d.sw = c.sw; d.ph = c.ph; d.pw = c.pw; d.dh = c.dh; d.dw = c.dw;
         d.G = c.G; d.Cg = (int)(c.C / c.G); d.Kg = (int)(c.K / c.G); d.Kgp = (int)pl.Kgp;
         d.in_nhwc = c.in_layout == AI3_NHWC; d.out_nhwc = c.out_layout == AI3_NHWC; d.bf16 = c.dtype == AI3_BF16;
-        e = launch_direct(d, st);
-        if (e != cudaSuccess) return cuda_fail(e, "direct kernel launch");
+        e = pl.algo == AI3_ALGO_SMM ? launch_smm(d, st) : launch_direct(d, st);
+        if (e != cudaSuccess) return cuda_fail(e, pl.algo == AI3_ALGO_SMM ? "smm kernel launch" : "direct kernel launch");
         return ok();
     }
     // 1. input preparation (layout / channel pad / operand precision)
@@ -574,6 +611,10 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = y;
+    } else if (pl.algo == AI3_ALGO_KN2ROW) {
+        if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
+        tp.args.out = w + pl.ws_M;
+        tp.args.bias = nullptr;
     } else if (pl.algo == AI3_ALGO_GEMM) {
         e = launch_im2col(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph,
                           c.pw, c.dh, c.dw, pl.Kp, pl.cm, w + pl.ws_A, w + pl.ws_Alo, st);
@@ -592,6 +633,12 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
     e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
+    if (pl.algo == AI3_ALGO_KN2ROW) {
+        e = launch_kn2row_accumulate(reinterpret_cast<const float*>(w + pl.ws_M), bias, y, c.out_layout == AI3_NHWC,
+                                     c.dtype == AI3_BF16, c.N, c.H, c.W, c.K, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw,
+                                     c.ph, c.pw, c.dh, c.dw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "kn2row shift-accumulate launch");
+    }
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,
                                    c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, st);
@@ -804,6 +851,8 @@ ai3_status ai3_conv2d(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* 
         return fail(AI3_ERR_SHAPE, "output tensor is (%lld,%lld,%lld,%lld), expected (%lld,%lld,%lld,%lld)",
                     (long long)y->n, (long long)y->c, (long long)y->h, (long long)y->w, (long long)os[0],
                     (long long)os[1], (long long)os[2], (long long)os[3]);
+    if (algo == AI3_ALGO_CUSTOM)
+        return ai3_conv2d_custom("custom", x, w, bias, stride, padding, dilation, groups, y, stream);
     ai3_plan* pl = nullptr;
     size_t wbytes = 0;
     if ((s = ai3_conv2d_plan_weight_bytes(&p, in_shape, (ai3_dtype)x->dtype, math, algo, &wbytes)) != AI3_OK) return s;

@@ -9,6 +9,9 @@
 
 namespace ai3 {
 
+// Set the thread-local ai3_last_error message and return `st` (api.cu).
+ai3_status api_fail(ai3_status st, const char* msg);
+
 // How the tensor-core algorithms multiply.
 enum ComputeMode : int {
     CM_BF16 = 0,   // bf16 operands, fp32 accumulate (tcgen05 kind::f16)
@@ -58,6 +61,18 @@ struct DirectArgs {
     int in_nhwc, out_nhwc, bf16;
 };
 cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st);
+// smm.cu: Scalar Matrix Multiplication (shifted zero-packed planes x scalar weights), same
+// argument block and prepared-weight layout as direct (Kgp a multiple of 16).
+cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- kn2row (kn2row.cu)
+// KCRS -> [(r*S+s)*K + k][Cpad] rows, compute mode (+ lo).
+cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
+                                       int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
+// Z fp32 [N*H*W][R*S*K] -> y (+bias): shift-accumulate of the R*S partial planes.
+cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
+                                     int64_t H, int64_t W, int64_t K, int64_t P, int64_t Q, int R, int S, int sh,
+                                     int sw, int ph, int pw, int dh, int dw, cudaStream_t st);
 
 // ---------------------------------------------------------------- im2col / winograd transforms
 // raw x (NCHW|NHWC, dtype) -> A[M][Kp] in compute mode (+ lo), columns (r, s, c) over the

@@ -1,0 +1,163 @@
+// smm.cu -- the `smm` algorithm: Scalar Matrix Multiplication with zero packing
+// (§II.B(c): "avoids matrix multiplications and replaces it with matrix
+// scaling operations.  Each output image can be considered as the summation of
+// shifted versions of the input image multiplied by the corresponding kernel
+// weight").
+//
+//   Y_k  =  b_k  +  sum_{c} sum_{r,s}  w[k][c][r][s] * shift_{r,s}(X_c)
+//
+// where shift_{r,s}(X_c)[p][q] = X_c[p*sh - ph + r*dh][q*sw - pw + s*dw] (zero outside:
+// the "zero packing" is the padded plane held in shared memory).  The loop order is
+// the algorithm's: input plane c outermost, then tap (r,s), then a scalar weight
+// broadcast times the shifted plane slice -- no reduction over channels inside a
+// matrix product.
+//
+// CUDA cores, fp32 FFMA.  One CTA (256 threads) owns an output tile of TP x TQ = 16 x 32
+// pixels of one image for KT = 16 output channels of one group.  Input planes are
+// staged PB at a time into shared memory with the padding zeros written in (zero
+// packing).  Each thread accumulates 2 pixels x 16 channels.
+// Any stride / padding / dilation / groups, NCHW or NHWC in and out, fp32 or bf16.
+#include <cuda_bf16.h>
+#include "internal.h"
+
+namespace ai3 {
+
+namespace {
+constexpr int KT = 16, TP = 16, TQ = 32, NT = 256;
+
+__device__ __forceinline__ float ld_act(const void* p, int64_t i, int bf16) {
+    return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
+}
+}  // namespace
+
+// w is the direct layout [G][Cg][R][S][Kgp] (fp32, k fastest): one tap of KT channels is
+// a contiguous 64-byte run, read as four broadcast float4 loads.
+template <int KS>
+__global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB, int FH, int FW, int FWp) {
+    extern __shared__ float smem[];
+    const int R = KS ? KS : a.R;
+    const int S = KS ? KS : a.S;
+    const int tid = threadIdx.x;
+    const int q = tid & 31;         // output column inside the tile
+    const int pr = tid >> 5;        // output rows pr and pr + 8
+    const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
+    const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
+    const int k0g = blockIdx.y * KT;
+    const int n = blockIdx.z / a.G, g = blockIdx.z % a.G;
+    const int ih0 = p0 * a.sh - a.ph, iw0 = q0 * a.sw - a.pw;
+    const int plane = FH * FWp;
+
+    float* xs = smem;                          // [PB][FH][FWp] zero-packed planes
+    float* wsm = smem + PB * plane;            // [PB][R][S][KT]
+
+    float acc[KT][2];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) acc[j][0] = acc[j][1] = 0.f;
+
+    const int64_t xsN = a.in_nhwc ? a.H * a.W * a.C : a.C * a.H * a.W;
+    const int64_t xsC = a.in_nhwc ? 1 : a.H * a.W;
+    const int64_t xsH = a.in_nhwc ? a.W * a.C : a.W;
+    const int64_t xsW = a.in_nhwc ? a.C : 1;
+    const int64_t xbase = (int64_t)n * xsN + (int64_t)g * a.Cg * xsC;
+
+    for (int c0 = 0; c0 < a.Cg; c0 += PB) {
+        const int pb = min(PB, a.Cg - c0);
+        // ---- zero-packed planes of channels c0 .. c0+pb-1 (padding written as zeros)
+        const int nx = pb * FH * FW;
+        for (int idx = tid; idx < nx; idx += NT) {
+            int cc, y, xw;
+            if (a.in_nhwc) { cc = idx % pb; const int t = idx / pb; xw = t % FW; y = t / FW; }
+            else { xw = idx % FW; const int t = idx / FW; y = t % FH; cc = t / FH; }
+            const int ih = ih0 + y, iw = iw0 + xw;
+            float v = 0.f;
+            if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
+                v = ld_act(a.x, xbase + (int64_t)(c0 + cc) * xsC + (int64_t)ih * xsH + (int64_t)iw * xsW, a.bf16);
+            xs[cc * plane + y * FWp + xw] = v;
+        }
+        // ---- the scalars: w[k0g .. k0g+KT)[c][r][s]
+        const int nw = pb * R * S * KT;
+        for (int idx = tid; idx < nw; idx += NT) {
+            const int kk = idx % KT;
+            const int t = idx / KT;  // (cc, r, s)
+            wsm[idx] = a.w[((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S + t) * a.Kgp + k0g + kk];
+        }
+        __syncthreads();
+        for (int cc = 0; cc < pb; ++cc) {
+            const float* X = xs + cc * plane;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    // shifted plane samples for this thread's two output pixels
+                    const int col = q * a.sw + s * a.dw;
+                    const float x0 = X[(pr * a.sh + r * a.dh) * FWp + col];
+                    const float x1 = X[((pr + 8) * a.sh + r * a.dh) * FWp + col];
+                    const float4* wv = reinterpret_cast<const float4*>(wsm + ((cc * R + r) * S + s) * KT);
+#pragma unroll
+                    for (int v = 0; v < KT / 4; ++v) {
+                        const float4 w4 = wv[v];  // broadcast: every thread reads the same scalars
+                        acc[4 * v + 0][0] = fmaf(w4.x, x0, acc[4 * v + 0][0]);
+                        acc[4 * v + 0][1] = fmaf(w4.x, x1, acc[4 * v + 0][1]);
+                        acc[4 * v + 1][0] = fmaf(w4.y, x0, acc[4 * v + 1][0]);
+                        acc[4 * v + 1][1] = fmaf(w4.y, x1, acc[4 * v + 1][1]);
+                        acc[4 * v + 2][0] = fmaf(w4.z, x0, acc[4 * v + 2][0]);
+                        acc[4 * v + 2][1] = fmaf(w4.z, x1, acc[4 * v + 2][1]);
+                        acc[4 * v + 3][0] = fmaf(w4.w, x0, acc[4 * v + 3][0]);
+                        acc[4 * v + 3][1] = fmaf(w4.w, x1, acc[4 * v + 3][1]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- bias once at the end, cast, store
+    const int qq = q0 + q;
+    if (qq >= a.Q) return;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int p = p0 + pr + 8 * h;
+        if (p >= a.P) break;
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            const int kk = k0g + j;
+            if (kk >= a.Kg) break;
+            const int64_t k = (int64_t)g * a.Kg + kk;
+            const float v = acc[j][h] + (a.bias ? a.bias[k] : 0.f);
+            const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + qq) * a.K + k
+                                         : (((int64_t)n * a.K + k) * a.P + p) * a.Q + qq;
+            if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
+            else reinterpret_cast<float*>(a.y)[o] = v;
+        }
+    }
+}
+
+// Kgp of the prepared weights must be a multiple of KT (the direct layout pads K per
+// group to 32, which is).
+cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st) {
+    const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
+    const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
+    int FWp = FW;
+    while (FWp % 32 != 1 && FWp % 32 != 17) ++FWp;  // rows pr and pr+8 of a warp in different banks
+    const int per_plane = (FH * FWp + a.R * a.S * KT) * 4;
+    int PB = (48 * 1024) / per_plane;
+    if (PB < 1) PB = 1;
+    if (PB > a.Cg) PB = a.Cg;
+    const size_t smem = (size_t)PB * per_plane;
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    if (a.Kgp % KT) return cudaErrorInvalidValue;
+    const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
+    dim3 grid(tiles, (unsigned)((a.Kg + KT - 1) / KT), (unsigned)(a.N * a.G));
+    if (grid.z > 65535) return cudaErrorInvalidConfiguration;
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, NT, smem, st>>>(a, PB, FH, FW, FWp);
+    };
+    if (a.R == a.S && a.R == 3) launch(smm_conv_kernel<3>);
+    else if (a.R == a.S && a.R == 1) launch(smm_conv_kernel<1>);
+    else if (a.R == a.S && a.R == 5) launch(smm_conv_kernel<5>);
+    else launch(smm_conv_kernel<0>);
+    return cudaGetLastError();
+}
+
+}  // namespace ai3

@@ -28,7 +28,7 @@ import torch
 from torch import nn
 
 from . import _lib
-from .conv import ConvPlan, UnknownAlgorithm, UnsupportedConfiguration, algo_id, layout_of
+from .conv import ConvPlan, UnknownAlgorithm, UnsupportedConfiguration, conv2d, layout_of, resolve
 
 Selector = Union[str, Sequence[str], Callable[[nn.Conv2d], str]]
 
@@ -53,8 +53,10 @@ def _conv_params(m: nn.Conv2d):
 
 def _validate(m: nn.Conv2d, algorithm: str, name: str = ""):
     """Swap-time check of the algorithm against the layer's hyperparameters."""
-    aid = algo_id(algorithm)  # raises UnknownAlgorithm
+    aid, custom = resolve(algorithm)  # raises UnknownAlgorithm
     stride, pad, dil, groups = _conv_params(m)
+    if custom is not None:
+        return custom  # what a user algorithm supports is its own business (PAPER.md:233)
     K, Cg, R, S = m.weight.shape
     C = Cg * groups
     # shape-independent constraints only: probe with an input just large enough
@@ -68,6 +70,7 @@ def _validate(m: nn.Conv2d, algorithm: str, name: str = ""):
         raise UnsupportedConfiguration(f"layer {name or m}: {_lib.last_error()}")
     if st == _lib.ERR_UNKNOWN_ALGORITHM:
         raise UnknownAlgorithm(_lib.last_error())
+    return None
 
 
 class Conv2D(nn.Module):
@@ -80,7 +83,7 @@ class Conv2D(nn.Module):
 
     def __init__(self, orig: nn.Conv2d, algorithm: str = "default", math: str = "strict", name: str = ""):
         super().__init__()
-        _validate(orig, algorithm, name)
+        self.custom = _validate(orig, algorithm, name)  # resolved registered name, or None
         self.weight = orig.weight
         self.bias = orig.bias
         self.in_channels, self.out_channels = orig.in_channels, orig.out_channels
@@ -112,6 +115,9 @@ class Conv2D(nn.Module):
             raise ValueError("ai3.Conv2D runs on CUDA tensors only (there is no CPU path)")
         if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
             x = x.contiguous()
+        if self.custom is not None:  # user algorithm: one ai3_conv2d_custom call per forward
+            return conv2d(x, self.weight, self.bias, self.stride, self.padding, self.dilation, self.groups,
+                          self.custom, self.math)
         return self.plan_for(x)(x)
 
 

@@ -20,6 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _header_functions():
     src = open(os.path.join(ROOT, "include", "ai3.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    src = re.sub(r"typedef[^;]*;", "", src, flags=re.S)  # function-pointer typedefs are not exports
     return sorted(set(re.findall(r"\b(ai3_[a-z0-9_]+)\s*\(", src)))
 
 
@@ -73,8 +74,17 @@ def test_winograd_preconditions():
     assert not ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="winograd")
 
 
+def test_smm_kn2row_preconditions():
+    """smm supports every conv direct does (groups too); kn2row needs groups == 1."""
+    for name in ("smm", "kn2row"):
+        assert ai3.supported((1, 8, 16, 16), 8, 3, padding=1, algorithm=name)
+        assert ai3.supported((2, 8, 16, 16), 8, 5, stride=2, dilation=2, padding=2, algorithm=name)
+    assert ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="smm")
+    assert not ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="kn2row")
+
+
 def test_reserved_algorithms_unsupported():
-    for name in ("smm", "kn2row", "implicit_precomp_gemm", "custom"):
+    for name in ("implicit_precomp_gemm",):
         with pytest.raises(ai3.UnsupportedConfiguration, match="reserved"):
             ai3.check_supported((1, 8, 16, 16), 8, 3, algorithm=name)
 

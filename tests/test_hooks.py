@@ -126,7 +126,8 @@ def _rel(a, b):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("sel,tol", [("direct", 1e-5), (["direct", "implicit_gemm"], 1e-5),
+@pytest.mark.parametrize("sel,tol", [("direct", 1e-5), (["direct", "implicit_gemm"], 1e-5), (["direct", "smm"], 1e-5),
+                                     ("kn2row", 1e-5),
                                      ("gemm", 1e-5), ("winograd", 1e-3), ("default", 1e-5)])
 def test_listing1_convnet(sel, tol):
     """randn(10,3,224,224) through swap_backend and swap_conv2d."""
@@ -146,7 +147,7 @@ def test_listing1_convnet(sel, tol):
 
 @pytest.mark.gpu
 def test_listing2_vgg16_rule_selector():
-    """PAPER.md:148-167 with random-init VGG16; "smm" (reserved here) -> implicit_gemm."""
+    """PAPER.md:148-167 (Listing 2) with random-init VGG16: "smm" for in_channels > 200, else "direct"."""
     torchvision = pytest.importorskip("torchvision")
     torch.manual_seed(0)
     vgg = torchvision.models.vgg16(weights=None).eval()
@@ -155,13 +156,13 @@ def test_listing2_vgg16_rule_selector():
     chosen = []
 
     def selector(orig: nn.Conv2d) -> str:
-        algo = "implicit_gemm" if orig.weight.shape[1] > 200 else "direct"
+        algo = "smm" if orig.weight.shape[1] > 200 else "direct"
         chosen.append(algo)
         return algo
 
     vgg = vgg.cuda()
     model = ai3.swap_backend(vgg, {"conv2d": selector})
-    assert chosen.count("implicit_gemm") == 8 and len(chosen) == 13
+    assert chosen.count("smm") == 8 and len(chosen) == 13
     with torch.inference_mode():
         out = model(x.cuda()).cpu().numpy()
     assert _rel(out, ref) <= 1e-4  # PAPER.md:163 atol=1e-4 analog (relative here)
