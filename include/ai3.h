@@ -75,8 +75,12 @@ typedef enum {
     AI3_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* "implicit_precomp_gemm" */
     AI3_ALGO_SMM = 6,               /* "smm": scalar matrix multiplication (§II.B(c)) */
     AI3_ALGO_KN2ROW = 7,            /* "kn2row": kernel-to-row 1x1 GEMMs + shift-accumulate (§II.B(b)) */
-    AI3_ALGO_CUSTOM = 8             /* "custom": the registered user algorithm (see below) */
+    AI3_ALGO_CUSTOM = 8,            /* "custom": the registered user algorithm (see below) */
+    AI3_ALGO_BENCHMARK = 9          /* "benchmark": the fastest algorithm measured by ai3_conv2d_autotune for this
+                                       problem (the `guess` rule until it has been measured) */
 } ai3_algo;
+
+#define AI3_NUM_ALGOS 10
 
 typedef enum { AI3_F32 = 0, AI3_BF16 = 1 } ai3_dtype;
 
@@ -203,6 +207,58 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
 /* Free the plan's host-side state (never the caller's device buffers). NULL is a no-op. */
 void ai3_conv2d_plan_destroy(ai3_plan* plan);
 
+/* Fused ReLU epilogue: after ai3_conv2d_plan_set_relu(plan, 1) every
+ * execute writes max(conv + bias, 0) (NaN propagates, as torch.relu) in the same kernel
+ * that stores the output -- the conv -> ReLU pair of an all-ai3 model costs one pass.
+ * Set before the plan's first use on a stream; 0 restores the plain convolution. */
+ai3_status ai3_conv2d_plan_set_relu(ai3_plan* plan, int32_t relu);
+
+/* ------------------------------------------------------------------ linear
+ *
+ * y[b][o] = bias[o] + sum_i x[b][i] * w[o][i]   (torch.nn.Linear; x [batch][in] row-major,
+ * w [out][in] row-major = PyTorch's layout, y [batch][out] row-major, one dtype).
+ * It is the 1x1 convolution of a batch of 1x1 images with `in` channels, and runs as one:
+ * the plan is a conv plan (NHWC, implicit GEMM on the tcgen05 engine), executed with
+ * ai3_conv2d_plan_execute(plan, x, y, workspace, bytes, stream) and freed with
+ * ai3_conv2d_plan_destroy.  Weight buffer / ownership / errors as ai3_conv2d_plan_create. */
+ai3_status ai3_linear_plan_weight_bytes(int64_t batch, int64_t in_features, int64_t out_features, int32_t has_bias,
+                                        ai3_dtype dtype, ai3_math math, size_t* bytes);
+ai3_status ai3_linear_plan_create(int64_t batch, int64_t in_features, int64_t out_features, ai3_dtype dtype,
+                                  ai3_math math, const void* w, const void* bias, void* weight_buf,
+                                  size_t weight_bytes, void* stream, ai3_plan** out);
+
+/* ------------------------------------------------------------------ other model operations
+ * (ReLU, max / average / adaptive-average pooling, flatten; PyTorch semantics so
+ * that a swap_backend model equals the original).  Device buffers, enqueued on
+ * `stream`; x and y share dtype and layout; descriptors use logical NCHW extents. */
+
+/* y = max(x, 0) elementwise over numel elements (x == y allowed).  NaN propagates. */
+ai3_status ai3_relu(const void* x, void* y, int64_t numel, int32_t dtype, void* stream);
+
+/* nn.MaxPool2d / nn.AvgPool2d hyperparameters. */
+typedef struct {
+    int32_t kernel[2];          /* kh, kw >= 1 */
+    int32_t stride[2];          /* >= 1 */
+    int32_t padding[2];         /* 0 <= padding <= kernel / 2 (torch's rule) */
+    int32_t dilation[2];        /* >= 1 (max pooling only; 1 for average pooling) */
+    int32_t ceil_mode;          /* output size rounds up; the last window must start inside input+left pad */
+    int32_t count_include_pad;  /* avg: divisor counts padding positions (torch default 1) */
+    int32_t divisor_override;   /* avg: 0 = none, else the divisor */
+} ai3_pool2d_params;
+
+/* out = {N, C, P, Q}: P = floor_or_ceil((H + 2p - d(k-1) - 1)/s) + 1 (torch's rule). */
+ai3_status ai3_pool2d_output_shape(const ai3_pool2d_params* params, const int64_t in_shape[4],
+                                   int64_t out_shape[4]);
+/* y[n][c][p][q] = max over window taps inside the input (padding never wins). */
+ai3_status ai3_maxpool2d(const ai3_tensor4d* x, const ai3_pool2d_params* params, ai3_tensor4d* y, void* stream);
+/* y = (sum over window taps inside the input) / divisor (see ai3_pool2d_params); fp32 sums. */
+ai3_status ai3_avgpool2d(const ai3_tensor4d* x, const ai3_pool2d_params* params, ai3_tensor4d* y, void* stream);
+/* nn.AdaptiveAvgPool2d((y->h, y->w)): rows [floor(i*H/P), ceil((i+1)*H/P)), columns likewise. */
+ai3_status ai3_adaptive_avgpool2d(const ai3_tensor4d* x, ai3_tensor4d* y, void* stream);
+/* Copy x into y's layout (NCHW <-> NHWC transpose, or a plain copy for equal layouts):
+ * the model's layout boundary and the NCHW order torch.flatten produces. */
+ai3_status ai3_layout_copy(const ai3_tensor4d* x, ai3_tensor4d* y, void* stream);
+
 /* ------------------------------------------------------------------ custom algorithms
  *
  * users implement their own convolution and select it "in the same
@@ -249,6 +305,29 @@ ai3_status ai3_conv2d_resolve(const char* name, ai3_algo* algo, char* custom_nam
 ai3_status ai3_conv2d_custom(const char* name, const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias,
                              const int32_t stride[2], const int32_t padding[2], const int32_t dilation[2],
                              int32_t groups, ai3_tensor4d* y, void* stream);
+
+/* ------------------------------------------------------------------ "benchmark" selection
+ *
+ * Time every built-in algorithm that supports the problem (direct, gemm, implicit_gemm,
+ * winograd -- not for fp32 STRICT, whose 1e-5 accuracy it cannot meet --, smm, kn2row) on
+ * the caller's buffers -- plan creation, one warm-up execute,
+ * then `reps` executes between CUDA events on `stream` -- and return the fastest in *best.
+ * ms_per_algo (optional, AI3_NUM_ALGOS floats indexed by ai3_algo) receives each
+ * algorithm's mean time, -1 for those not run.  BLOCKS the host (synchronises `stream`).
+ * x, w (KCRS), bias (or NULL), y: device buffers as for ai3_conv2d_plan_execute in the
+ * given layouts; y is overwritten.  scratch: device, 256-byte aligned; algorithms whose
+ * prepared weights + workspace exceed scratch_bytes are skipped (size it with
+ * ai3_conv2d_autotune_scratch_bytes to run all).  The winner is cached per (problem,
+ * dtype, math, layouts); AI3_ALGO_BENCHMARK then resolves to it everywhere. */
+ai3_status ai3_conv2d_autotune_scratch_bytes(const ai3_conv2d_params* params, const int64_t in_shape[4],
+                                             ai3_dtype dtype, ai3_math math, int32_t in_layout,
+                                             int32_t out_layout, size_t* bytes);
+ai3_status ai3_conv2d_autotune(const ai3_conv2d_params* params, const int64_t in_shape[4], ai3_dtype dtype,
+                               ai3_math math, int32_t in_layout, int32_t out_layout, const void* x,
+                               const void* w, const void* bias, void* y, void* scratch, size_t scratch_bytes,
+                               int32_t reps, void* stream, ai3_algo* best, float* ms_per_algo);
+/* Forget every cached autotune result. */
+void ai3_conv2d_autotune_clear(void);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,8 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE", 3: "UNSUPPORTED", 4:
                 5: "WORKSPACE", 6: "CUDA"}
 # ai3_algo
 ALGO_GUESS, ALGO_DIRECT, ALGO_GEMM, ALGO_IMPLICIT_GEMM, ALGO_WINOGRAD = 0, 1, 2, 3, 4
-ALGO_IMPLICIT_PRECOMP_GEMM, ALGO_SMM, ALGO_KN2ROW, ALGO_CUSTOM = 5, 6, 7, 8
+ALGO_IMPLICIT_PRECOMP_GEMM, ALGO_SMM, ALGO_KN2ROW, ALGO_CUSTOM, ALGO_BENCHMARK = 5, 6, 7, 8, 9
+NUM_ALGOS = 10
 # ai3_dtype / ai3_math / ai3_layout
 F32, BF16 = 0, 1
 MATH_STRICT, MATH_TF32 = 0, 1
@@ -31,7 +32,11 @@ EXPORTS = ["ai3_version", "ai3_last_error", "ai3_algo_name", "ai3_algo_from_name
            "ai3_conv2d_plan_weight_bytes", "ai3_conv2d_plan_create", "ai3_conv2d_plan_algo",
            "ai3_conv2d_plan_workspace_size", "ai3_conv2d_plan_num_launches", "ai3_conv2d_plan_execute",
            "ai3_conv2d_plan_execute_host", "ai3_conv2d_plan_destroy", "ai3_register_conv2d",
-           "ai3_unregister_conv2d", "ai3_custom_conv2d_count", "ai3_conv2d_resolve", "ai3_conv2d_custom"]
+           "ai3_unregister_conv2d", "ai3_custom_conv2d_count", "ai3_conv2d_resolve", "ai3_conv2d_custom",
+           "ai3_conv2d_plan_set_relu", "ai3_linear_plan_weight_bytes", "ai3_linear_plan_create", "ai3_relu",
+           "ai3_pool2d_output_shape", "ai3_maxpool2d", "ai3_avgpool2d", "ai3_adaptive_avgpool2d",
+           "ai3_layout_copy", "ai3_conv2d_autotune_scratch_bytes", "ai3_conv2d_autotune",
+           "ai3_conv2d_autotune_clear"]
 
 
 class Ai3LibraryMissing(RuntimeError):
@@ -47,6 +52,12 @@ class Params(ctypes.Structure):
 class Tensor4d(ctypes.Structure):
     _fields_ = [("data", ctypes.c_void_p), ("n", ctypes.c_int64), ("c", ctypes.c_int64), ("h", ctypes.c_int64),
                 ("w", ctypes.c_int64), ("dtype", ctypes.c_int32), ("layout", ctypes.c_int32)]
+
+
+class PoolParams(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32 * 2), ("stride", ctypes.c_int32 * 2), ("padding", ctypes.c_int32 * 2),
+                ("dilation", ctypes.c_int32 * 2), ("ceil_mode", ctypes.c_int32),
+                ("count_include_pad", ctypes.c_int32), ("divisor_override", ctypes.c_int32)]
 
 
 # ai3_conv2d_custom_fn (include/ai3.h)
@@ -100,6 +111,24 @@ def load():
         "ai3_conv2d_resolve": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, sz], ctypes.c_int),
         "ai3_conv2d_custom": ([ctypes.c_char_p, ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), vp, i32x2, i32x2,
                                i32x2, i32, ctypes.POINTER(Tensor4d), vp], ctypes.c_int),
+        "ai3_conv2d_plan_set_relu": ([vp, i32], ctypes.c_int),
+        "ai3_linear_plan_weight_bytes": ([i64, i64, i64, i32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(sz)],
+                                         ctypes.c_int),
+        "ai3_linear_plan_create": ([i64, i64, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp, sz, vp,
+                                    ctypes.POINTER(vp)], ctypes.c_int),
+        "ai3_relu": ([vp, vp, i64, i32, vp], ctypes.c_int),
+        "ai3_pool2d_output_shape": ([ctypes.POINTER(PoolParams), i64x4, i64x4], ctypes.c_int),
+        "ai3_maxpool2d": ([ctypes.POINTER(Tensor4d), ctypes.POINTER(PoolParams), ctypes.POINTER(Tensor4d), vp],
+                          ctypes.c_int),
+        "ai3_avgpool2d": ([ctypes.POINTER(Tensor4d), ctypes.POINTER(PoolParams), ctypes.POINTER(Tensor4d), vp],
+                          ctypes.c_int),
+        "ai3_adaptive_avgpool2d": ([ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), vp], ctypes.c_int),
+        "ai3_layout_copy": ([ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), vp], ctypes.c_int),
+        "ai3_conv2d_autotune_scratch_bytes": ([pp, i64x4, ctypes.c_int, ctypes.c_int, i32, i32, ctypes.POINTER(sz)],
+                                              ctypes.c_int),
+        "ai3_conv2d_autotune": ([pp, i64x4, ctypes.c_int, ctypes.c_int, i32, i32, vp, vp, vp, vp, vp, sz, i32, vp,
+                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+        "ai3_conv2d_autotune_clear": ([], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

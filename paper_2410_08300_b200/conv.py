@@ -13,8 +13,8 @@ import torch
 
 from . import _lib
 
-ALGORITHMS = ("guess", "default", "auto", "direct", "gemm", "im2col", "implicit_gemm", "winograd", "smm", "kn2row",
-              "implicit_precomp_gemm", "custom")
+ALGORITHMS = ("guess", "default", "auto", "benchmark", "direct", "gemm", "im2col", "implicit_gemm", "winograd", "smm",
+              "kn2row", "implicit_precomp_gemm", "custom")
 
 
 class Ai3Error(RuntimeError):
@@ -229,6 +229,40 @@ def conv2d(input: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None 
     return out
 
 
+def autotune(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = None, stride=1, padding=0,
+             dilation=1, groups: int = 1, math: str = "strict", reps: int = 3, out_layout=None):
+    """Time every built-in algorithm that supports this convolution on these tensors
+    (ai3_conv2d_autotune) and return (fastest name, {name: ms}).  The winner is cached, so
+    the algorithm name "benchmark" then selects it for this problem."""
+    _require_cuda(x, weight, bias)
+    lib = _lib.load()
+    if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
+        x = x.contiguous()
+    weight = weight.detach().to(x.dtype).contiguous()
+    if bias is not None:
+        bias = bias.detach().to(x.dtype).contiguous()
+    in_layout = layout_of(x)
+    out_layout = in_layout if out_layout is None else out_layout
+    s, p, d = _pair(stride), _pair(padding), _pair(dilation)
+    prm = _lib.params(weight.shape[0], weight.shape[2:], s, p, d, groups, bias is not None)
+    shp = _lib.shape4(x.shape)
+    nbytes = ctypes.c_size_t()
+    _check(lib.ai3_conv2d_autotune_scratch_bytes(ctypes.byref(prm), shp, _dtype_id(x.dtype), _math_id(math),
+                                                 in_layout, out_layout, ctypes.byref(nbytes)))
+    scratch = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=x.device)
+    oshape = output_shape(x.shape, weight.shape[0], weight.shape[2:], s, p, d, groups)
+    fmt = torch.channels_last if out_layout == _lib.NHWC else torch.contiguous_format
+    y = torch.empty(oshape, dtype=x.dtype, device=x.device, memory_format=fmt)
+    best = ctypes.c_int()
+    ms = (ctypes.c_float * _lib.NUM_ALGOS)()
+    with torch.cuda.device(x.device):
+        _check(lib.ai3_conv2d_autotune(ctypes.byref(prm), shp, _dtype_id(x.dtype), _math_id(math), in_layout,
+                                       out_layout, x.data_ptr(), weight.data_ptr(),
+                                       None if bias is None else bias.data_ptr(), y.data_ptr(), scratch.data_ptr(),
+                                       scratch.numel(), int(reps), _stream_ptr(x.device), ctypes.byref(best), ms))
+    return algo_name(best.value), {algo_name(i): float(ms[i]) for i in range(_lib.NUM_ALGOS) if ms[i] >= 0}
+
+
 class ConvPlan:
     """Weights prepared once (swap time) for one input shape / layout / dtype.
 
@@ -291,6 +325,12 @@ class ConvPlan:
                                                    0 if ws is None else ws.numel(), _stream_ptr(self.device)))
         self._keep = None
         return out
+
+    def set_relu(self, relu: bool = True) -> "ConvPlan":
+        """Fuse a ReLU into the plan's output epilogue (ai3_conv2d_plan_set_relu)."""
+        _check(_lib.load().ai3_conv2d_plan_set_relu(self._h, 1 if relu else 0))
+        self.relu = bool(relu)
+        return self
 
     def execute_raw(self, x_ptr: int, y_ptr: int, ws_ptr: int | None, ws_bytes: int, stream_ptr: int):
         """Bare C-ABI call on raw device pointers (benchmarks, dispatch-overhead check)."""

@@ -43,7 +43,7 @@ const NameEntry kNames[] = {
     {"direct", AI3_ALGO_DIRECT}, {"gemm", AI3_ALGO_GEMM}, {"im2col", AI3_ALGO_GEMM},
     {"implicit_gemm", AI3_ALGO_IMPLICIT_GEMM}, {"winograd", AI3_ALGO_WINOGRAD},
     {"implicit_precomp_gemm", AI3_ALGO_IMPLICIT_PRECOMP_GEMM}, {"smm", AI3_ALGO_SMM},
-    {"kn2row", AI3_ALGO_KN2ROW}, {"custom", AI3_ALGO_CUSTOM},
+    {"kn2row", AI3_ALGO_KN2ROW}, {"custom", AI3_ALGO_CUSTOM}, {"benchmark", AI3_ALGO_BENCHMARK},
 };
 
 // ---------------------------------------------------------------- problem validation
@@ -112,6 +112,7 @@ int tiled_row_bytes(int64_t kred_bytes) { return kred_bytes >= 128 ? 128 : (kred
 ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
     switch (algo) {
         case AI3_ALGO_GUESS:
+        case AI3_ALGO_BENCHMARK:
         case AI3_ALGO_DIRECT:
             return ok();
         case AI3_ALGO_IMPLICIT_GEMM: {
@@ -188,10 +189,14 @@ ai3_algo guess_rule(const ConvProblem& c) {
 }
 
 ai3_status resolve_algo(const ConvProblem& c, ai3_algo algo, ai3_algo* out) {
-    if ((int)algo < 0 || (int)algo > (int)AI3_ALGO_CUSTOM)
+    if ((int)algo < 0 || (int)algo >= AI3_NUM_ALGOS)
         return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
     ai3_status s = check_supported(c, algo);
     if (s != AI3_OK) return s;
+    if (algo == AI3_ALGO_BENCHMARK) {
+        if (!autotune_lookup(c, out)) *out = guess_rule(c);  // not measured yet: the shape rule
+        return ok();
+    }
     *out = algo == AI3_ALGO_GUESS ? guess_rule(c) : algo;
     return ok();
 }
@@ -228,6 +233,7 @@ struct ai3_plan {
     const void* cached_out = nullptr;
     CUtensorMap tout{};
     int launches = 1;
+    int relu = 0;  // fused ReLU epilogue (ai3_conv2d_plan_set_relu)
 };
 
 namespace {
@@ -588,6 +594,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         d.R = (int)c.R; d.S = (int)c.S; d.sh = c.sh; d.sw = c.sw; d.ph = c.ph; d.pw = c.pw; d.dh = c.dh; d.dw = c.dw;
         d.G = c.G; d.Cg = (int)(c.C / c.G); d.Kg = (int)(c.K / c.G); d.Kgp = (int)pl.Kgp;
         d.in_nhwc = c.in_layout == AI3_NHWC; d.out_nhwc = c.out_layout == AI3_NHWC; d.bf16 = c.dtype == AI3_BF16;
+        d.relu = pl.relu;
         e = pl.algo == AI3_ALGO_SMM ? launch_smm(d, st) : launch_direct(d, st);
         if (e != cudaSuccess) return cuda_fail(e, pl.algo == AI3_ALGO_SMM ? "smm kernel launch" : "direct kernel launch");
         return ok();
@@ -607,6 +614,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     std::lock_guard<std::mutex> lock(pl.mu);
     TcPlan tp = pl.tc;
     tp.args.bias = bias;
+    tp.args.relu = pl.relu;  // the GEMM's output is y (implicit_gemm, gemm); cleared below otherwise
     ai3_status s;
     if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
@@ -615,6 +623,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = w + pl.ws_M;
         tp.args.bias = nullptr;
+        tp.args.relu = 0;
     } else if (pl.algo == AI3_ALGO_GEMM) {
         e = launch_im2col(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph,
                           c.pw, c.dh, c.dw, pl.Kp, pl.cm, w + pl.ws_A, w + pl.ws_Alo, st);
@@ -628,6 +637,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         if ((s = encode_a_maps(pl, w + pl.ws_V, w + pl.ws_Vlo)) != AI3_OK) return s;
         tp.args.out = w + pl.ws_M;
         tp.args.bias = nullptr;
+        tp.args.relu = 0;
     }
     if (tp.args.stg_row && !aligned(tp.args.out, 16)) tp.args.stg_row = 0;  // TMA needs a 16-byte base
     if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
@@ -636,12 +646,12 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if (pl.algo == AI3_ALGO_KN2ROW) {
         e = launch_kn2row_accumulate(reinterpret_cast<const float*>(w + pl.ws_M), bias, y, c.out_layout == AI3_NHWC,
                                      c.dtype == AI3_BF16, c.N, c.H, c.W, c.K, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw,
-                                     c.ph, c.pw, c.dh, c.dw, st);
+                                     c.ph, c.pw, c.dh, c.dw, pl.relu, st);
         if (e != cudaSuccess) return cuda_fail(e, "kn2row shift-accumulate launch");
     }
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,
-                                   c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, st);
+                                   c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);
         if (e != cudaSuccess) return cuda_fail(e, "winograd output transform launch");
     }
     return ok();
@@ -680,6 +690,7 @@ const char* ai3_algo_name(ai3_algo algo) {
         case AI3_ALGO_SMM: return "smm";
         case AI3_ALGO_KN2ROW: return "kn2row";
         case AI3_ALGO_CUSTOM: return "custom";
+        case AI3_ALGO_BENCHMARK: return "benchmark";
     }
     return "?";
 }
@@ -689,7 +700,8 @@ ai3_status ai3_algo_from_name(const char* name, ai3_algo* out) {
     for (const NameEntry& e : kNames)
         if (std::strcmp(e.name, name) == 0) { *out = e.algo; return ok(); }
     return fail(AI3_ERR_UNKNOWN_ALGORITHM,
-                "unknown algorithm '%s' (known: guess, default, auto, direct, gemm, im2col, implicit_gemm, winograd)",
+                "unknown algorithm '%s' (known: guess, default, auto, benchmark, direct, gemm, im2col, implicit_gemm, "
+                "winograd, smm, kn2row, custom, or a registered custom name)",
                 name);
 }
 
@@ -819,6 +831,43 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
 }
 
 void ai3_conv2d_plan_destroy(ai3_plan* plan) { delete plan; }
+
+// Linear = 1x1 convolution of `batch` 1x1 images with in_features channels, NHWC in/out
+// (the [batch][in] / [batch][out] row-major buffers), on the tcgen05 implicit GEMM.
+static void linear_params(int64_t out_features, int32_t has_bias, ai3_conv2d_params* p) {
+    std::memset(p, 0, sizeof *p);
+    p->out_channels = out_features;
+    p->kernel[0] = p->kernel[1] = 1;
+    p->stride[0] = p->stride[1] = 1;
+    p->dilation[0] = p->dilation[1] = 1;
+    p->groups = 1;
+    p->has_bias = has_bias ? 1 : 0;
+}
+
+ai3_status ai3_linear_plan_weight_bytes(int64_t batch, int64_t in_features, int64_t out_features, int32_t has_bias,
+                                        ai3_dtype dtype, ai3_math math, size_t* bytes) {
+    ai3_conv2d_params p;
+    linear_params(out_features, has_bias, &p);
+    const int64_t in_shape[4] = {batch, in_features, 1, 1};
+    return ai3_conv2d_plan_weight_bytes(&p, in_shape, dtype, math, AI3_ALGO_IMPLICIT_GEMM, bytes);
+}
+
+ai3_status ai3_linear_plan_create(int64_t batch, int64_t in_features, int64_t out_features, ai3_dtype dtype,
+                                  ai3_math math, const void* w, const void* bias, void* weight_buf,
+                                  size_t weight_bytes, void* stream, ai3_plan** out) {
+    ai3_conv2d_params p;
+    linear_params(out_features, bias != nullptr, &p);
+    const int64_t in_shape[4] = {batch, in_features, 1, 1};
+    return ai3_conv2d_plan_create(&p, in_shape, dtype, math, AI3_ALGO_IMPLICIT_GEMM, AI3_NHWC, AI3_NHWC, w, bias,
+                                  weight_buf, weight_bytes, stream, out);
+}
+
+ai3_status ai3_conv2d_plan_set_relu(ai3_plan* plan, int32_t relu) {
+    if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    plan->relu = relu ? 1 : 0;
+    return ok();
+}
 
 ai3_status ai3_conv2d(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias, const int32_t stride[2],
                       const int32_t padding[2], const int32_t dilation[2], int32_t groups, ai3_algo algo,

@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
             if (q >= a.Q) break;
             const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + q) * a.K + k
                                          : (((int64_t)n * a.K + k) * a.P + p) * a.Q + q;
-            const float v = acc[j][i] + bv;
+            float v = acc[j][i] + bv;
+            if (a.relu && v < 0.f) v = 0.f;
             if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
             else reinterpret_cast<float*>(a.y)[o] = v;
         }

@@ -12,6 +12,10 @@ namespace ai3 {
 // Set the thread-local ai3_last_error message and return `st` (api.cu).
 ai3_status api_fail(ai3_status st, const char* msg);
 
+struct ConvProblem;
+// The algorithm ai3_conv2d_autotune measured fastest for this problem, if any (autotune.cu).
+bool autotune_lookup(const ConvProblem& c, ai3_algo* out);
+
 // How the tensor-core algorithms multiply.
 enum ComputeMode : int {
     CM_BF16 = 0,   // bf16 operands, fp32 accumulate (tcgen05 kind::f16)
@@ -59,6 +63,7 @@ struct DirectArgs {
     int64_t N, C, H, W, K, P, Q;
     int R, S, sh, sw, ph, pw, dh, dw, G, Cg, Kg, Kgp;
     int in_nhwc, out_nhwc, bf16;
+    int relu;             // fused ReLU after the bias
 };
 cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st);
 // smm.cu: Scalar Matrix Multiplication (shifted zero-packed planes x scalar weights), same
@@ -72,7 +77,7 @@ cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K
 // Z fp32 [N*H*W][R*S*K] -> y (+bias): shift-accumulate of the R*S partial planes.
 cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
                                      int64_t H, int64_t W, int64_t K, int64_t P, int64_t Q, int R, int S, int sh,
-                                     int sw, int ph, int pw, int dh, int dw, cudaStream_t st);
+                                     int sw, int ph, int pw, int dh, int dw, int relu, cudaStream_t st);
 
 // ---------------------------------------------------------------- im2col / winograd transforms
 // raw x (NCHW|NHWC, dtype) -> A[M][Kp] in compute mode (+ lo), columns (r, s, c) over the
@@ -92,7 +97,7 @@ cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W
                                   cudaStream_t st);
 // M (fp32, [16][K][T] if out NCHW else [16][T][K]) -> y (+bias), cropped to P x Q.
 cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
-                                   int64_t N, int64_t K, int64_t P, int64_t Q, cudaStream_t st);
+                                   int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 engine (tc_engine.cu)
 enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2, TC_A_HALO = 3 };
@@ -131,6 +136,7 @@ struct TcArgs {
     int bias_smem;  // 1: the epilogue stages the fp32 bias in shared memory
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
+    int relu;       // 1: fused ReLU after the bias (model path)
     const float* bias;  // fp32 [Ncols] or null
     void* out;
     long long out_bstride;  // elements between batches

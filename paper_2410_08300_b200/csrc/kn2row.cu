@@ -67,7 +67,7 @@ template <int VK>
 __global__ void kn2row_accumulate_kernel(const float* __restrict__ Z, const float* __restrict__ bias, void* y,
                                          int out_nhwc, int bf16, int64_t N, int64_t H, int64_t W, int64_t K,
                                          int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh,
-                                         int dw) {
+                                         int dw, int relu) {
     const int64_t kg = K / VK;
     const int64_t total = N * P * Q * kg;
     const int64_t zrow = (int64_t)R * S * K;
@@ -97,7 +97,8 @@ __global__ void kn2row_accumulate_kernel(const float* __restrict__ Z, const floa
 #pragma unroll
         for (int v = 0; v < VK; ++v) {
             const int64_t k = k0 + v;
-            const float val = acc[v] + (bias ? bias[k] : 0.f);
+            float val = acc[v] + (bias ? bias[k] : 0.f);
+            if (relu && val < 0.f) val = 0.f;
             const int64_t o = out_nhwc ? m * K + k : ((n * K + k) * P + p) * Q + q;
             if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(val);
             else reinterpret_cast<float*>(y)[o] = val;
@@ -107,16 +108,16 @@ __global__ void kn2row_accumulate_kernel(const float* __restrict__ Z, const floa
 
 cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
                                      int64_t H, int64_t W, int64_t K, int64_t P, int64_t Q, int R, int S, int sh,
-                                     int sw, int ph, int pw, int dh, int dw, cudaStream_t st) {
+                                     int sw, int ph, int pw, int dh, int dw, int relu, cudaStream_t st) {
     const int VK = K % 4 == 0 ? 4 : 1;
     const int64_t total = N * P * Q * (K / VK);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
     if (VK == 4)
         kn2row_accumulate_kernel<4><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S, sh, sw,
-                                                          ph, pw, dh, dw);
+                                                          ph, pw, dh, dw, relu);
     else
         kn2row_accumulate_kernel<1><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S, sh, sw,
-                                                          ph, pw, dh, dw);
+                                                          ph, pw, dh, dw, relu);
     return cudaGetLastError();
 }
 

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB
     const int plane = FH * FWp;
 
     float* xs = smem;                          // [PB][FH][FWp] zero-packed planes
-    float* wsm = smem + PB * plane;            // [PB][R][S][KT]
+    float* wsm = smem + ((PB * plane + 3) & ~3);  // [PB][R][S][KT], 16-byte aligned for float4 loads
 
     float acc[KT][2];
 #pragma unroll
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB
             const int kk = k0g + j;
             if (kk >= a.Kg) break;
             const int64_t k = (int64_t)g * a.Kg + kk;
-            const float v = acc[j][h] + (a.bias ? a.bias[k] : 0.f);
+            float v = acc[j][h] + (a.bias ? a.bias[k] : 0.f);
+            if (a.relu && v < 0.f) v = 0.f;
             const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + qq) * a.K + k
                                          : (((int64_t)n * a.K + k) * a.P + p) * a.Q + qq;
             if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
@@ -143,7 +144,7 @@ cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st) {
     int PB = (48 * 1024) / per_plane;
     if (PB < 1) PB = 1;
     if (PB > a.Cg) PB = a.Cg;
-    const size_t smem = (size_t)PB * per_plane;
+    const size_t smem = (size_t)PB * per_plane + 16;
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     if (a.Kgp % KT) return cudaErrorInvalidValue;
     const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));

@@ -531,6 +531,10 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                         f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
                     }
                 }
+                if (a.relu) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
+                }
                 const int half = BOX64 ? hh : 0;
                 const uint32_t buf = stg_u32 + slot * 32 * ROWB;
                 if (half == 0 && issued >= n_stg) {  // slot reuse: that store must have read smem
@@ -717,6 +721,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int j = 0; j < 32; ++j)
                         if (col0 + j < a.Ncols) f[j] += a.bias[col0 + j];
                 }
+            }
+            if (a.relu) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];
             }
             if (a.stg_row == 0 || a.store_mode == 0) {
                 if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);

@@ -305,7 +305,7 @@ cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W
 //         m_kt = 0 -> [16][T][K] (threads walk k fastest, NHWC stores coalesce).
 __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, const float* __restrict__ bias, void* y,
                                        int out_nhwc, int bf16, int64_t N, int64_t K, int64_t P, int64_t Q,
-                                       int64_t TH, int64_t TW) {
+                                       int64_t TH, int64_t TW, int relu) {
     const int64_t T = N * TH * TW;
     const int64_t total = T * K;
     const int64_t plane = T * K;
@@ -341,20 +341,21 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
                 const int64_t q = 2 * tw + b;
                 if (q >= Q) break;
                 const int64_t o = out_nhwc ? ((n * P + p) * Q + q) * K + k : ((n * K + k) * P + p) * Q + q;
-                if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(yv[a][b]);
-                else reinterpret_cast<float*>(y)[o] = yv[a][b];
+                const float v = (relu && yv[a][b] < 0.f) ? 0.f : yv[a][b];
+                if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(v);
+                else reinterpret_cast<float*>(y)[o] = v;
             }
         }
     }
 }
 
 cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
-                                   int64_t N, int64_t K, int64_t P, int64_t Q, cudaStream_t st) {
+                                   int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st) {
     const int64_t TH = (P + 1) / 2, TW = (Q + 1) / 2;
     const int64_t total = N * TH * TW * K;
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
-    winograd_output_kernel<<<grid, 256, 0, st>>>(M, m_kt, bias, y, out_nhwc, bf16, N, K, P, Q, TH, TW);
+    winograd_output_kernel<<<grid, 256, 0, st>>>(M, m_kt, bias, y, out_nhwc, bf16, N, K, P, Q, TH, TW, relu);
     return cudaGetLastError();
 }
 

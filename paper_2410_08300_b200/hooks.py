@@ -92,6 +92,7 @@ class Conv2D(nn.Module):
         self.algorithm = algorithm
         self.math = math
         self.layer_name = name
+        self.relu = False  # fused ReLU epilogue (set by swap_backend for conv -> relu pairs)
         self._plans = {}
 
     def extra_repr(self):
@@ -104,8 +105,13 @@ class Conv2D(nn.Module):
         key = (tuple(x.shape), x.dtype, lay, x.device)
         ent = self._plans.get(key)
         if ent is None or ent[0] != wv:
+            if self.algorithm == "benchmark":  # measure every algorithm once for this shape
+                from .conv import autotune
+                autotune(x, self.weight, self.bias, self.stride, self.padding, self.dilation, self.groups, self.math)
             plan = ConvPlan(self.weight, self.bias, x.shape, self.stride, self.padding, self.dilation, self.groups,
                             self.algorithm, self.math, in_layout=lay, dtype=x.dtype)
+            if self.relu:
+                plan.set_relu(True)
             ent = (wv, plan)
             self._plans[key] = ent
         return ent[1]
@@ -116,8 +122,12 @@ class Conv2D(nn.Module):
         if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
             x = x.contiguous()
         if self.custom is not None:  # user algorithm: one ai3_conv2d_custom call per forward
-            return conv2d(x, self.weight, self.bias, self.stride, self.padding, self.dilation, self.groups,
-                          self.custom, self.math)
+            y = conv2d(x, self.weight, self.bias, self.stride, self.padding, self.dilation, self.groups,
+                       self.custom, self.math)
+            if self.relu:
+                from .layers import relu
+                y = relu(y, inplace=True)
+            return y
         return self.plan_for(x)(x)
 
 
@@ -178,35 +188,83 @@ def swap_conv2d(module: nn.Module, algos: Selector = "default", math: str = "str
 
 
 class Model(nn.Module):
-    """Result of ``swap_backend``: the traced graph of the original
-    module with each conv2d bound to its selected ai3 algorithm.
+    """Result of ``swap_backend`` ("returns an object completely
+    managed by the framework"): the traced graph of the original module with every
+    supported module and function replaced by ai3's (conv2d with its selected algorithm,
+    linear, ReLU, max / average / adaptive-average pooling, flatten).
 
-    Scope note: ai3 kernels cover conv2d, the hot path; the other
-    traced operations (pooling, activations, linear, flatten) still execute through
-    the graph as PyTorch ops -- the all-ai3 operator set is SURVEY §8 row f1.
+    Activations run NHWC (channels_last) end to end: 4-D inputs are converted once at
+    entry by ai3's layout kernel.  Conv -> ReLU pairs run as one kernel (fused epilogue);
+    flatten -> linear reads the NHWC activation directly.  ``cuda_graph=True`` captures
+    the forward per input shape in a CUDA graph after one eager warm-up call and replays
+    it (static input/output buffers; the returned tensor is overwritten by the next call).
     """
 
-    def __init__(self, graph_module: nn.Module, layers):
+    def __init__(self, graph_module: nn.Module, layers, replaced=(), kept=(), cuda_graph: bool = False):
         super().__init__()
         self.graph_module = graph_module
-        self.layers = layers  # [(qualname, algorithm)] in trace order
+        self.layers = layers          # [(qualname, algorithm)] of the convolutions, in trace order
+        self.replaced = list(replaced)  # [(node, ai3 op)] everything swapped
+        self.kept = list(kept)          # [(node, target)] left as PyTorch (unsupported by ai3)
+        self.cuda_graph = cuda_graph
+        self._graphs = {}
 
-    def forward(self, *args, **kwargs):
-        return self.graph_module(*args, **kwargs)
+    def _eager(self, *args):
+        from .layers import to_layout
+        args = tuple(to_layout(a, _lib.NHWC) if isinstance(a, torch.Tensor) and a.dim() == 4 and a.is_cuda
+                     and a.is_floating_point() else a for a in args)
+        return self.graph_module(*args)
+
+    def forward(self, *args):
+        if not self.cuda_graph or not all(isinstance(a, torch.Tensor) and a.is_cuda for a in args):
+            return self._eager(*args)
+        key = tuple((tuple(a.shape), a.dtype, a.device, a.stride()) for a in args)
+        ent = self._graphs.get(key)
+        if ent is None:
+            out = self._eager(*args)  # warm-up: plans, weight preparation, workspaces
+            torch.cuda.current_stream().synchronize()
+            static_in = [a.clone() for a in args]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                static_out = self._eager(*static_in)
+            self._graphs[key] = (g, static_in, static_out)
+            return out
+        g, static_in, static_out = ent
+        for s, a in zip(static_in, args):
+            s.copy_(a)
+        g.replay()
+        return static_out
 
 
-def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None, math: str = "strict") -> Model:
-    """Build an ``ai3.Model`` from ``module``.  ``algos`` maps an
-    operation name to a selector; only "conv2d" is algorithm-selectable."""
+def _is_fn(target, *fns):
+    return any(target is f for f in fns)
+
+
+def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None, math: str = "strict",
+                 cuda_graph: bool = False) -> Model:
+    """Build an ``ai3.Model`` from ``module``.
+
+    Every supported PyTorch module and function of the traced graph is replaced by ai3's
+    implementation; ``algos`` maps an operation name to a selector and only "conv2d" is
+    algorithm-selectable (the other operations have one implementation each).
+    Operations ai3 does not implement stay PyTorch ops and are listed in ``Model.kept``.
+    Dropout is the identity in the inference graph and is removed.
+    """
+    import copy
+    import operator
+
+    import torch.nn.functional as F
+
+    from . import layers as L
+
     algos = dict(algos or {})
     unknown = set(algos) - {"conv2d"}
     if unknown:
         raise UnknownAlgorithm(f"no selectable operation named {sorted(unknown)} (supported: conv2d)")
     sel = algos.get("conv2d", "default")
-    import copy
-    gm = torch.fx.symbolic_trace(copy.deepcopy(module))
+    gm = torch.fx.symbolic_trace(copy.deepcopy(module).eval())
     order = _traced_conv_order(gm)
-    layers = []
+    layers, replaced, kept = [], [], []
     for i, qn in enumerate(order):
         conv = gm.get_submodule(qn)
         name = _resolve(sel, conv, i)
@@ -214,5 +272,100 @@ def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None,
             raise UnsupportedConfiguration("'torch' is only valid for swap_conv2d (PAPER.md:170)")
         _set_submodule(gm, qn, Conv2D(conv, name, math, qn))
         layers.append((qn, name))
+        replaced.append((qn, "conv2d:" + name))
+
+    graph = gm.graph
+    mods = dict(gm.named_modules())
+    for node in list(graph.nodes):
+        if node.op == "call_module":
+            m = mods[node.target]
+            new = None
+            if isinstance(m, (Conv2D, L.ReLU, L.MaxPool2D, L.AvgPool2D, L.AdaptiveAvgPool2D, L.Flatten, L.Linear)):
+                continue  # already swapped (a module called more than once)
+            if isinstance(m, nn.ReLU):
+                new = L.ReLU()
+            elif isinstance(m, nn.MaxPool2d):
+                new = L.MaxPool2D(m)
+            elif isinstance(m, nn.AvgPool2d):
+                new = L.AvgPool2D(m)
+            elif isinstance(m, nn.AdaptiveAvgPool2d):
+                new = L.AdaptiveAvgPool2D(m)
+            elif isinstance(m, nn.Flatten):
+                new = L.Flatten(m)
+            elif isinstance(m, nn.Linear):
+                new = L.Linear(m, math)
+            elif isinstance(m, (nn.Dropout, nn.Identity)):
+                node.replace_all_uses_with(node.args[0])
+                graph.erase_node(node)
+                replaced.append((node.target, "identity"))
+                continue
+            if new is None:
+                kept.append((node.target, type(m).__name__))
+                continue
+            _set_submodule(gm, node.target, new)
+            mods[node.target] = new
+            replaced.append((node.target, type(new).__name__))
+        elif node.op == "call_function" or node.op == "call_method":
+            t = node.target
+            if node.op == "call_function" and _is_fn(t, torch.relu, F.relu, torch.relu_):
+                node.target = L.relu
+                node.kwargs = {k: v for k, v in node.kwargs.items() if k != "inplace"}
+                if len(node.args) > 1:
+                    node.args = node.args[:1]
+            elif node.op == "call_function" and _is_fn(t, torch.flatten):
+                node.target = L.flatten
+            elif node.op == "call_function" and _is_fn(t, F.max_pool2d):
+                node.target = L.max_pool2d
+            elif node.op == "call_function" and _is_fn(t, F.avg_pool2d):
+                node.target = L.avg_pool2d
+            elif node.op == "call_function" and _is_fn(t, F.adaptive_avg_pool2d):
+                node.target = L.adaptive_avg_pool2d
+            elif node.op == "call_method" and t == "relu":
+                node.op, node.target = "call_function", L.relu
+            elif node.op == "call_function" and _is_fn(t, F.dropout):
+                node.replace_all_uses_with(node.args[0])
+                graph.erase_node(node)
+                replaced.append((node.name, "identity"))
+                continue
+            elif node.op == "call_function" and t in (operator.getitem, getattr):
+                continue
+            else:
+                kept.append((node.name, getattr(t, "__name__", str(t))))
+                continue
+            replaced.append((node.name, node.target.__name__))
+
+    # fusion: conv2d / linear -> relu (sole consumer) runs as one kernel (fused epilogue)
+    def _mod(n):
+        return mods.get(n.target) if n.op == "call_module" else None
+
+    def _is_relu(n):
+        return (n.op == "call_function" and n.target is L.relu) or isinstance(_mod(n), L.ReLU)
+
+    for node in list(graph.nodes):
+        if not _is_relu(node) or not node.args or not isinstance(node.args[0], torch.fx.Node):
+            continue
+        src = node.args[0]
+        producer = _mod(src)
+        if isinstance(producer, (Conv2D, L.Linear)) and len(src.users) == 1 and not producer.relu:
+            producer.relu = True
+            node.replace_all_uses_with(src)
+            graph.erase_node(node)
+            replaced.append((src.name, "fused_relu"))
+
+    # fusion: flatten(NHWC) -> linear reads the activation in place (weight columns permuted once)
+    for node in list(graph.nodes):
+        is_flat = (node.op == "call_function" and node.target is L.flatten) or isinstance(_mod(node), L.Flatten)
+        if not is_flat or len(node.users) != 1:
+            continue
+        user = next(iter(node.users))
+        start_dim = node.args[1] if len(node.args) > 1 else node.kwargs.get("start_dim", 1)
+        if isinstance(_mod(node), L.Flatten):
+            start_dim = _mod(node).start_dim
+        if isinstance(_mod(user), L.Linear) and start_dim == 1 and user.args[0] is node:
+            user.args = (node.args[0],) + tuple(user.args[1:])
+            graph.erase_node(node)
+            replaced.append((user.name, "flatten_fused"))
+
+    graph.lint()
     gm.recompile()
-    return Model(gm, layers)
+    return Model(gm, layers, replaced, kept, cuda_graph)

@@ -16,9 +16,10 @@ for checking only; it is timed separately and excluded from images/s (north_star
 Timing: barrier -> CUDA events around the forward on each rank -> all_reduce(MAX)
 -> images/s = N / t_max.
 
-The non-convolution layers (ReLU, max-pool, adaptive avg-pool, linear) run as
-PyTorch ops, as after the paper's swap_conv2d; the all-ai3 operator set is
-SURVEY §8 row f1.
+By default the model is swap_backend's all-ai3 model (SURVEY §8 row
+f1): conv + ReLU fused, ai3 max-pool, flatten fused into the first linear, linear
+layers on the tcgen05 engine.  --swap conv2d swaps only the convolutions
+and --swap none runs PyTorch, for comparison.
 """
 from __future__ import annotations
 
@@ -52,14 +53,18 @@ def make_images(lo: int, hi: int, seed: int, device, dtype=torch.bfloat16, size:
     return out.to(dtype).contiguous(memory_format=torch.channels_last)
 
 
-def build_vgg16(device, dtype=torch.bfloat16, algo="guess", seed: int = 0, swap: bool = True):
+def build_vgg16(device, dtype=torch.bfloat16, algo="guess", seed: int = 0, swap: str = "backend"):
     """torchvision VGG-16 with random-init weights (no network for pretrained ones), identical
-    on every rank (same seed), convolutions swapped to ai3."""
+    on every rank (same seed).  swap="backend": swap_backend, every op in ai3 (PAPER.md:142);
+    "conv2d": swap_conv2d, only the convolutions; "none": PyTorch."""
     import torchvision
     torch.manual_seed(seed)
     model = torchvision.models.vgg16(weights=None).eval()
     model = model.to(device=device, dtype=dtype).to(memory_format=torch.channels_last)
-    if swap:
+    if swap == "backend":
+        from .hooks import swap_backend
+        return swap_backend(model, {"conv2d": algo})
+    if swap == "conv2d":
         from .hooks import swap_conv2d
         swap_conv2d(model, algo)
     return model
@@ -85,7 +90,7 @@ def max_over_ranks(value: float, device) -> float:
     return float(t.item())
 
 
-def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check: bool):
+def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check: bool, swap: str = "backend"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -95,7 +100,7 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
         dist.init_process_group("nccl", device_id=device)
     lo, hi = shard_bounds(global_batch, world, rank)
     x = make_images(lo, hi, seed + 1, device)
-    model = build_vgg16(device, algo=algo, seed=seed)
+    model = build_vgg16(device, algo=algo, seed=seed, swap=swap)
     with torch.inference_mode():
         for _ in range(warmup):
             y = model(x)
@@ -112,7 +117,7 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
     if world > 1:
         ms = max_over_ranks(ms, device)
     result = {"global_batch": global_batch, "n_gpus": world, "ms_per_forward": ms,
-              "images_per_s": global_batch / (ms * 1e-3), "algo": algo}
+              "images_per_s": global_batch / (ms * 1e-3), "algo": algo, "swap": swap}
     if world > 1:
         counts = [shard_bounds(global_batch, world, r)[1] - shard_bounds(global_batch, world, r)[0]
                   for r in range(world)]
@@ -123,24 +128,22 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
     else:
         logits = y.float()
     if check:
-        # sharding changes nothing: for sampled images of this rank's slab, the conv stack's
-        # features computed alone equal the batched ones bit for bit (ai3 kernels reduce in a
-        # batch-independent order; ReLU / max-pool are per element).  The torch linear
-        # layers may pick batch-size-dependent cuBLAS kernels, so logits get a tolerance.
+        # sharding changes nothing: sampled images of this rank's slab run alone give the same
+        # logits, bit for bit (every ai3 kernel reduces each output in an order that does not
+        # depend on the batch; ReLU / pooling are per element).
         idx = sorted({lo, (lo + hi) // 2, hi - 1})
         ok, worst = True, 0.0
         with torch.inference_mode():
-            feats = model.features(x)
             for i in idx:
                 xi = make_images(i, i + 1, seed + 1, device)
-                ok &= bool(torch.equal(model.features(xi), feats[i - lo:i - lo + 1]))
                 yi = model(xi).float()
+                ok &= bool(torch.equal(yi, logits[i:i + 1]))
                 worst = max(worst, float((yi - logits[i:i + 1]).abs().max()))
         flags = torch.tensor([1.0 if ok else 0.0, worst], dtype=torch.float64, device=device)
         if world > 1:
             dist.all_reduce(flags[:1], op=dist.ReduceOp.MIN)
             dist.all_reduce(flags[1:], op=dist.ReduceOp.MAX)
-        result["features_bit_identical_when_sharded"] = bool(flags[0].item() == 1.0)
+        result["logits_bit_identical_when_sharded"] = bool(flags[0].item() == 1.0)
         result["logits_max_abs_diff_vs_single_image"] = float(flags[1].item())
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -157,8 +160,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=5000)
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--swap", default="backend", choices=["backend", "conv2d", "none"])
     a = ap.parse_args()
-    run(a.global_batch, a.algo, a.steps, a.warmup, a.seed, not a.no_check)
+    run(a.global_batch, a.algo, a.steps, a.warmup, a.seed, not a.no_check, a.swap)
 
 
 if __name__ == "__main__":
