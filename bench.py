@@ -292,11 +292,39 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "path": "ai3_conv2d_plan_execute_host per layer, pinned host memory"}
         del hx, hy
 
+    # ---- the whole model: swap_backend(VGG-16), every op in ai3 (BASELINE configs[4]'s model
+    #      at this rank's batch), timed the same way; reported beside the conv-stack metric
+    model_leg = None
+    if not args.no_model:
+        from paper_2410_08300_b200.runner import build_vgg16, make_images
+        try:
+            model = build_vgg16(device, algo=args.algo, seed=0, swap="backend")
+            xm = make_images(0, BATCH, 5001, device)
+            with torch.inference_mode():
+                for _ in range(3):
+                    model(xm)
+                torch.cuda.synchronize(device)
+                s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = max(3, min(args.steps, 20))
+                s0.record(stream)
+                for _ in range(reps):
+                    model(xm)
+                e0.record(stream)
+                e0.synchronize()
+            mms = s0.elapsed_time(e0) / reps
+            model_leg = {"model": "vgg16 (torchvision, random init), swap_backend: all ops in ai3", "batch": BATCH,
+                         "ms_per_forward": mms, "images_per_s": BATCH / (mms * 1e-3),
+                         "ops_kept_in_torch": len(model.kept)}
+            del model, xm
+            torch.cuda.empty_cache()
+        except Exception as ex:  # report, do not hide
+            model_leg = {"error": str(ex)}
+
     # ---- per-algorithm comparison on the same stack (config: Winograd vs implicit GEMM vs direct)
     per_algo = None
     if not args.no_compare and rank == 0:
         per_algo = {}
-        for algo in ("implicit_gemm", "winograd", "gemm", "kn2row", "direct", "smm"):
+        for algo in ("implicit_gemm", "implicit_precomp_gemm", "winograd", "gemm", "kn2row", "direct", "smm"):
             if algo == args.algo:
                 per_algo[algo] = round(value / world, 1)
                 continue
@@ -330,7 +358,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                            "l2": "step working set ~2.9 GB of distinct per-layer buffers >> 126 MB L2; no flush"},
                 "images_per_s": images_per_s, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "per_layer": per_layer,
-                "per_algorithm_tflops": per_algo}
+                "per_algorithm_tflops": per_algo, "vgg16_model": model_leg}
         print(json.dumps(line), flush=True)
 
 
@@ -344,6 +372,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-model", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -160,7 +160,11 @@ ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
                 return fail(AI3_ERR_UNSUPPORTED, "'custom' selected but no custom conv2d algorithm is registered");
             return ok();
         case AI3_ALGO_IMPLICIT_PRECOMP_GEMM:
-            return fail(AI3_ERR_UNSUPPORTED, "algorithm '%s' is reserved and not built yet", ai3_algo_name(algo));
+            if (c.G != 1)
+                return fail(AI3_ERR_UNSUPPORTED, "implicit_precomp_gemm requires groups == 1 (got %d); use direct", c.G);
+            if (c.N * c.H * c.W >= (1LL << 31) || c.N * c.P * c.Q + 256 >= (1LL << 31))
+                return fail(AI3_ERR_UNSUPPORTED, "implicit_precomp_gemm: N*H*W or N*P*Q >= 2^31");
+            return ok();
     }
     return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
 }
@@ -224,6 +228,8 @@ struct ai3_plan {
     int64_t Kgp = 0;  // direct: padded K per group
     // workspace regions (byte offsets)
     size_t ws_x = 0, ws_xlo = 0, ws_A = 0, ws_Alo = 0, ws_V = 0, ws_Vlo = 0, ws_M = 0, ws_bytes = 0;
+    size_t idx_off = 0;     // implicit_precomp_gemm: row table in the weight buffer
+    int64_t idx_rows = 0;
     // engine
     TcPlan tc{};
     CUtensorMap tb0{}, tb1{};
@@ -295,6 +301,11 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     if (pl.splits == 2) off = align_up(off + wcount * e);
     pl.bias_off = off;
     if (c.has_bias) off = align_up(off + (size_t)c.K * 4);
+    if (algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
+        pl.idx_rows = round_up(c.N * c.P * c.Q, 256);
+        pl.idx_off = off;
+        off = align_up(off + (size_t)c.R * c.S * pl.idx_rows * 4);
+    }
     pl.wbytes = off;
 
     // input preparation pass
@@ -346,6 +357,14 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
             const char* e = getenv("AI3_HALO_BO");
             a.halo_bo = (e && e[0] == '1') ? 1 : 0;
         }
+        pl.launches = 1 + (pl.need_prep ? 1 : 0);
+    } else if (algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
+        a.a_mode = TC_A_GATHER;
+        a.M = (int)M;
+        a.row_bytes = implicit_row_bytes(pl.Cpad, pl.elem);
+        a.c_chunks = (int)(pl.Cpad * pl.elem / a.row_bytes);
+        a.num_kb = (int)(c.R * c.S * a.c_chunks);
+        a.gather_rows = (int)pl.idx_rows;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_GEMM) {
         a.a_mode = TC_A_IM2COL;
@@ -491,6 +510,13 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         const uint32_t es[4] = {1, (uint32_t)c.sw, (uint32_t)c.sh, 1};
         oka = encode_im2col(&pl.ta0, dt, src, dims, str, lower, upper, kel, 128, es, sw);
         if (oka && pl.splits == 2) oka = encode_im2col(&pl.ta1, dt, src_lo, dims, str, lower, upper, kel, 128, es, sw);
+    } else if (pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
+        // rows of the NHWC input [N*H*W][Cpad]; one gather4 = 4 rows x one K-block chunk
+        const uint64_t dims[2] = {(uint64_t)pl.Cpad, (uint64_t)(c.N * c.H * c.W)};
+        const uint64_t str[1] = {(uint64_t)pl.Cpad * e};
+        const uint32_t box[2] = {kel, 1};
+        oka = encode_tiled(&pl.ta0, dt, 2, src, dims, str, box, sw);
+        if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 2, src_lo, dims, str, box, sw);
     } else if (pl.algo == AI3_ALGO_GEMM || pl.algo == AI3_ALGO_KN2ROW) {
         const uint64_t kred = (uint64_t)pl.Kp;
         const uint64_t dims[2] = {kred, (uint64_t)a.M};
@@ -571,6 +597,12 @@ ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaSt
         e = launch_pack_weights(w, c.dtype, c.K, c.C, c.R, c.S, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
     }
     if (e != cudaSuccess) return cuda_fail(e, "weight preparation launch");
+    if (pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
+        e = launch_gather_table(reinterpret_cast<int*>(wb + pl.idx_off), c.N * c.P * c.Q, pl.idx_rows, c.H, c.W, c.P,
+                                c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph, c.pw, c.dh, c.dw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "gather table launch");
+        pl.tc.args.gather_idx = reinterpret_cast<const int*>(wb + pl.idx_off);
+    }
     if (pl.bias_present) {
         e = launch_bias_f32(bias, c.dtype, c.K, reinterpret_cast<float*>(wb + pl.bias_off), st);
         if (e != cudaSuccess) return cuda_fail(e, "bias preparation launch");
@@ -616,7 +648,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     tp.args.bias = bias;
     tp.args.relu = pl.relu;  // the GEMM's output is y (implicit_gemm, gemm); cleared below otherwise
     ai3_status s;
-    if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
+    if (pl.algo == AI3_ALGO_IMPLICIT_GEMM || pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = y;
     } else if (pl.algo == AI3_ALGO_KN2ROW) {

@@ -1,12 +1,18 @@
 // direct.cu -- the `direct` algorithm (§II.B(d): "kernels are applied
 // directly to the input without transforming the data").
 //
-// CUDA-core FFMA with fp32 accumulation.  One CTA (256 threads) computes a tile of
-// 32 output channels x (8 rows x 32 columns) output pixels of one image / group.
-// Per channel chunk the CTA stages the input footprint and the 32 channels'
-// weights in shared memory (k fastest, so a thread's 8 weights are two
-// broadcast 128-bit loads); each thread then accumulates 8 channels x 4
-// pixels = 32 fp32 accumulators over (c, r, s) in that order.
+// CUDA-core FFMA with fp32 accumulation; bound by the FP32 pipe (VGG/ResNet
+// layers have >= 16 flop/byte against an 11.5 flop/byte FFMA ridge).
+//
+// One CTA (256 threads, 8 warps) computes 32 output channels x (8 rows x 64 columns)
+// output pixels of one image / group.  Per chunk of CB input channels the CTA stages the
+// zero-padded input footprint and the chunk's weights ([cc][r][s][32 k], k fastest) in
+// shared memory.  Each thread owns an 8-channel x 8-pixel register tile (one output row,
+// 8 consecutive columns; 64 fp32 accumulators).  Per (channel, filter row) it reads its
+// input row segment once -- 128-bit loads for stride 1 -- and slides it across the S
+// filter columns in registers; the 8 weights of a tap are two broadcast 128-bit loads
+// (every lane of a warp shares its k group).  That is 64 FFMA per 2 weight loads plus
+// (8 + S - 1)/4 input loads: the FP32 pipe, not shared memory, is the limit.
 // Handles any stride / padding / dilation / groups and NCHW or NHWC, fp32 or bf16.
 #include <cuda_bf16.h>
 #include "internal.h"
@@ -14,34 +20,37 @@
 namespace ai3 {
 
 namespace {
-constexpr int TK = 32, TP = 8, TQ = 32, NT = 256;
+constexpr int TK = 32, TP = 8, TQ = 64, NT = 256, VQ = 8;
 
 __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
 }
 }  // namespace
 
-template <int KS>
-__global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp, int xs_floats) {
-    extern __shared__ float smem[];
+// KS: compile-time square kernel size (0 = runtime R, S).  UNIT: stride 1 and dilation 1
+// along w (the row segment is loaded with 128-bit loads and slid in registers).
+template <int KS, bool UNIT>
+__global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
+                                                            int xs_floats) {
+    extern __shared__ __align__(16) float smem[];
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
     const int tid = threadIdx.x;
-    const int qg = tid & 7, pr = (tid >> 3) & 7, kg = tid >> 6;
+    const int qg = tid & 7, pr = (tid >> 3) & 7, kg = tid >> 6;  // a warp: one k group, 4 rows x 8 column groups
     const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
     const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
     const int k0g = blockIdx.y * TK;
     const int n = blockIdx.z / a.G, g = blockIdx.z % a.G;
     const int ih0 = p0 * a.sh - a.ph, iw0 = q0 * a.sw - a.pw;
 
-    float* xs = smem;                         // [CB][FH][FWp]
-    float* ws = smem + xs_floats;  // [CB][R][S][TK], 16-byte aligned for float4 loads
+    float* xs = smem;              // [CB][FH][FWp]
+    float* ws = smem + xs_floats;  // [CB][R][S][TK]
 
-    float acc[8][4];
+    float acc[8][VQ];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
+        for (int i = 0; i < VQ; ++i) acc[j][i] = 0.f;
 
     const int64_t xsN = a.in_nhwc ? a.H * a.W * a.C : a.C * a.H * a.W;
     const int64_t xsC = a.in_nhwc ? 1 : a.H * a.W;
@@ -51,7 +60,7 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
 
     for (int c0 = 0; c0 < a.Cg; c0 += CB) {
         const int cb = min(CB, a.Cg - c0);
-        // ---- stage input footprint
+        // ---- stage the input footprint (zeros outside the image)
         const int nx = cb * FH * FW;
         for (int idx = tid; idx < nx; idx += NT) {
             int cc, y, xw;
@@ -74,29 +83,52 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
         for (int cc = 0; cc < cb; ++cc) {
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
-                const float* xrow = xs + (cc * FH + pr * a.sh + rr * a.dh) * FWp + qg * 4 * a.sw;
+                const float* xrow = xs + (cc * FH + pr * a.sh + rr * a.dh) * FWp + qg * VQ * a.sw;
                 const float* wrow = ws + ((cc * R + rr) * S) * TK + kg * 8;
+                if (UNIT && KS) {
+                    // row segment xrow[0 .. VQ + S - 2] read once (16-byte aligned: FWp % 4 == 0,
+                    // qg * VQ % 4 == 0) and slid across the S filter columns in registers
+                    constexpr int NSEG = (VQ + (KS ? KS : 1) - 1 + 3) / 4;
+                    float xr[NSEG * 4];
 #pragma unroll
-                for (int ss = 0; ss < S; ++ss) {
-                    const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
-                    const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
-                    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-                    float xv[4];
+                    for (int v = 0; v < NSEG; ++v) {
+                        const float4 t = *reinterpret_cast<const float4*>(xrow + 4 * v);
+                        xr[4 * v] = t.x; xr[4 * v + 1] = t.y; xr[4 * v + 2] = t.z; xr[4 * v + 3] = t.w;
+                    }
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[i] = xrow[i * a.sw + ss * a.dw];
+                    for (int ss = 0; ss < S; ++ss) {
+                        const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
+                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
+                        for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) acc[j][i] = fmaf(wv[j], xv[i], acc[j][i]);
+                            for (int i = 0; i < VQ; ++i) acc[j][i] = fmaf(wv[j], xr[i + ss], acc[j][i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int ss = 0; ss < S; ++ss) {
+                        const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
+                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                        float xv[VQ];
+#pragma unroll
+                        for (int i = 0; i < VQ; ++i) xv[i] = xrow[i * a.sw + ss * a.dw];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int i = 0; i < VQ; ++i) acc[j][i] = fmaf(wv[j], xv[i], acc[j][i]);
+                    }
                 }
             }
         }
         __syncthreads();
     }
 
-    // ---- epilogue: bias once at the end, cast, store
+    // ---- epilogue: bias once at the end, optional ReLU, cast, store
     const int p = p0 + pr;
     if (p >= a.P) return;
+    const int qb = q0 + qg * VQ;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int kk = k0g + kg * 8 + j;
@@ -104,13 +136,13 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
         const int64_t k = (int64_t)g * a.Kg + kk;
         const float bv = a.bias ? a.bias[k] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int q = q0 + qg * 4 + i;
+        for (int i = 0; i < VQ; ++i) {
+            const int q = qb + i;
             if (q >= a.Q) break;
-            const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + q) * a.K + k
-                                         : (((int64_t)n * a.K + k) * a.P + p) * a.Q + q;
             float v = acc[j][i] + bv;
             if (a.relu && v < 0.f) v = 0.f;
+            const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + q) * a.K + k
+                                         : (((int64_t)n * a.K + k) * a.P + p) * a.Q + q;
             if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
             else reinterpret_cast<float*>(a.y)[o] = v;
         }
@@ -118,12 +150,15 @@ __global__ void __launch_bounds__(NT) direct_conv_kernel(const DirectArgs a, int
 }
 
 cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
+    const bool unit = a.sw == 1 && a.dw == 1;
     const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
-    int FWp = FW;
-    while (FWp % 4 != 1) ++FWp;  // row stride = 1 mod 4: the 4 rows of a warp hit distinct banks
+    // 16-byte aligned rows; unit-stride segments may read up to 3 floats past FW (zeroed
+    // region never used for the result: loads beyond VQ + S - 1 are discarded)
+    int FWp = (FW + 3 + 3) / 4 * 4;
+    if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
     const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
-    const int budget = 64 * 1024;
+    const int budget = 48 * 1024;
     int CB = budget / per_c;
     if (CB < 1) CB = 1;
     if (CB > a.Cg) CB = a.Cg;
@@ -132,16 +167,25 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
     dim3 grid(tiles, (unsigned)((a.Kg + TK - 1) / TK), (unsigned)(a.N * a.G));
+    if (grid.z > 65535) return cudaErrorInvalidConfiguration;
     auto launch = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp, xs_floats);
     };
-    if (a.R == a.S && a.R == 3) launch(direct_conv_kernel<3>);
-    else if (a.R == a.S && a.R == 1) launch(direct_conv_kernel<1>);
-    else if (a.R == a.S && a.R == 5) launch(direct_conv_kernel<5>);
-    else if (a.R == a.S && a.R == 7) launch(direct_conv_kernel<7>);
-    else if (a.R == a.S && a.R == 11) launch(direct_conv_kernel<11>);
-    else launch(direct_conv_kernel<0>);
+    const bool sq = a.R == a.S;
+    if (unit) {
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, true>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true>);
+        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true>);
+        else if (sq && a.R == 7) launch(direct_conv_kernel<7, true>);
+        else launch(direct_conv_kernel<0, true>);
+    } else {
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, false>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false>);
+        else if (sq && a.R == 7) launch(direct_conv_kernel<7, false>);
+        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false>);
+        else launch(direct_conv_kernel<0, false>);
+    }
     return cudaGetLastError();
 }
 

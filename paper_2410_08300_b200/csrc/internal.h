@@ -51,6 +51,9 @@ cudaError_t launch_winograd_filter(const void* w, ai3_dtype dtype, int64_t K, in
 // KCRS (grouped: K x Cg x R x S) -> fp32 [G][Cg][R][S][Kgp] (k fastest, zero padded).
 cudaError_t launch_direct_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t Cg, int64_t R, int64_t S,
                                   int G, int64_t Kgp, float* dst, cudaStream_t st);
+// implicit_precomp_gemm row table [R*S][rows] (int32, -1 = zero padding).
+cudaError_t launch_gather_table(int* idx, int64_t M, int64_t rows, int64_t H, int64_t W, int64_t P, int64_t Q, int R,
+                                int S, int sh, int sw, int ph, int pw, int dh, int dw, cudaStream_t st);
 // bias (dtype) -> fp32
 cudaError_t launch_bias_f32(const void* b, ai3_dtype dtype, int64_t K, float* dst, cudaStream_t st);
 
@@ -100,7 +103,7 @@ cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, 
                                    int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 engine (tc_engine.cu)
-enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2, TC_A_HALO = 3 };
+enum TcAMode : int { TC_A_IM2COL = 0, TC_A_TILED2D = 1, TC_A_TILED3D = 2, TC_A_HALO = 3, TC_A_GATHER = 4 };
 
 struct TcArgs {
     int a_mode;     // TcAMode
@@ -137,6 +140,10 @@ struct TcArgs {
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
     int relu;       // 1: fused ReLU after the bias (model path)
+    // gather mode (a_mode == TC_A_GATHER, implicit_precomp_gemm): precomputed input-row table
+    // [R*S][m_rows] int32 (row of the NHWC [N*H*W][Cpad] view, -1 = padding -> zero fill)
+    const int* gather_idx;
+    int gather_rows;  // m_rows: the table's row pitch (>= m_tiles * 128 * cg)
     const float* bias;  // fp32 [Ncols] or null
     void* out;
     long long out_bstride;  // elements between batches

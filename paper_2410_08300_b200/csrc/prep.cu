@@ -228,6 +228,34 @@ cudaError_t launch_direct_weights(const void* w, ai3_dtype dtype, int64_t K, int
     return cudaGetLastError();
 }
 
+// implicit_precomp_gemm: idx[tap][m] = row (n*H + ih)*W + iw of the NHWC
+// input that output pixel m reads at filter tap (r, s), or -1 where that tap falls in the
+// zero padding (and for m >= M, the last tile's tail).  Shape-only: built once per plan.
+__global__ void gather_table_kernel(int* __restrict__ idx, int64_t M, int64_t rows, int64_t H, int64_t W, int64_t P,
+                                    int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw) {
+    const int64_t total = (int64_t)R * S * rows;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i % rows;
+        const int tap = (int)(i / rows);
+        const int r = tap / S, s = tap % S;
+        int v = -1;
+        if (m < M) {
+            const int64_t n = m / (P * Q), pq = m % (P * Q);
+            const int64_t ih = (pq / Q) * sh - ph + (int64_t)r * dh, iw = (pq % Q) * sw - pw + (int64_t)s * dw;
+            if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = (int)((n * H + ih) * W + iw);
+        }
+        idx[i] = v;
+    }
+}
+
+cudaError_t launch_gather_table(int* idx, int64_t M, int64_t rows, int64_t H, int64_t W, int64_t P, int64_t Q, int R,
+                                int S, int sh, int sw, int ph, int pw, int dh, int dw, cudaStream_t st) {
+    const int64_t total = (int64_t)R * S * rows;
+    const int grid = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+    gather_table_kernel<<<grid, 256, 0, st>>>(idx, M, rows, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw);
+    return cudaGetLastError();
+}
+
 __global__ void bias_f32_kernel(const void* __restrict__ b, int bf16, int64_t K, float* __restrict__ dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = load_as_f32(b, i, bf16);

@@ -208,6 +208,64 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
     }
 }
 
+// ---------------------------------------------------------------- gather producer (one warp)
+// implicit_precomp_gemm: the A tile of K-block (tap, channel chunk) is the
+// 128 input rows a precomputed table names for this tile's output pixels at that tap;
+// each lane gathers 4 of them with one TMA gather4 (rows of -1 -> zero fill = padding).
+template <int CG>
+__device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorMap& ta0, const CUtensorMap& ta1,
+                                                const CUtensorMap& tb0, const CUtensorMap& tb1, uint8_t* smem,
+                                                uint64_t* full, uint64_t* empty, uint32_t rank, int unit,
+                                                int num_units, int lane) {
+    const bool leader = rank == 0;
+    const int splits = a.cm == CM_3XTF32 ? 2 : 1;
+    const int bn_cta = a.block_n / CG;
+    const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
+    const int tiles_per_batch = a.m_tiles * a.n_tiles;
+    const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = unit; tile < tiles_per_batch; tile += num_units) {
+        const int mt = tile / a.n_tiles;
+        const int m0 = mt * (BM * CG) + (int)rank * BM;
+        const int n0 = (tile - mt * a.n_tiles) * a.block_n + (int)rank * bn_cta;
+        int cc = 0, tap = 0;
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+            if (lane == 0) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (CG == 1) mbar_arrive_expect_tx(&full[stage], stage_bytes);
+                else if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+            }
+            __syncwarp();
+            uint8_t* sA = smem + stage * stage_bytes;
+            uint8_t* sB = sA + splits * a_bytes;
+            const int4 r = *reinterpret_cast<const int4*>(a.gather_idx + (size_t)tap * a.gather_rows + m0 + 4 * lane);
+            const int cx = cc * kelems;
+            uint8_t* dA = sA + lane * 4 * a.row_bytes;
+            if (CG == 1) {
+                tma_gather4(dA, &ta0, &full[stage], cx, r.x, r.y, r.z, r.w);
+                if (splits == 2) tma_gather4(dA + a_bytes, &ta1, &full[stage], cx, r.x, r.y, r.z, r.w);
+                if (lane == 0) {
+                    tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
+                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
+                }
+            } else {
+                const uint32_t bar = full_base + stage * 8;
+                tma_gather4_cg2(dA, &ta0, bar, cx, r.x, r.y, r.z, r.w);
+                if (splits == 2) tma_gather4_cg2(dA + a_bytes, &ta1, bar, cx, r.x, r.y, r.z, r.w);
+                if (lane == 0) {
+                    tma_load_2d_cg2(sB, &tb0, bar, kb * kelems, n0);
+                    if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kb * kelems, n0);
+                }
+            }
+            if (++cc == a.c_chunks) { cc = 0; ++tap; }
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- MMA issuer (one thread)
 // The K loop of a tile is split into accumulation chunks of `promote_kb` K-blocks (the
 // whole loop unless 3xTF32); each chunk goes to one of the two TMEM buffers and is handed
@@ -619,7 +677,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int unit = blockIdx.x / CG, num_units = gridDim.x / CG;  // tile scheduler works per CTA group
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
-    if (warp == 0) {
+    if (warp == 0 && a.a_mode == TC_A_GATHER) {
+        producer_gather<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units, lane);
+        __syncwarp();
+    } else if (warp == 0) {
         if (elect_one()) {
             TRACE_WAIT(1, {
                 if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);

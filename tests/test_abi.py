@@ -83,10 +83,12 @@ def test_smm_kn2row_preconditions():
     assert not ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="kn2row")
 
 
-def test_reserved_algorithms_unsupported():
-    for name in ("implicit_precomp_gemm",):
-        with pytest.raises(ai3.UnsupportedConfiguration, match="reserved"):
-            ai3.check_supported((1, 8, 16, 16), 8, 3, algorithm=name)
+def test_every_named_algorithm_is_built():
+    """No reserved names remain: each selectable name resolves to a built algorithm."""
+    for name in ("direct", "gemm", "im2col", "implicit_gemm", "implicit_precomp_gemm", "winograd", "smm", "kn2row",
+                 "guess", "auto", "default", "benchmark"):
+        assert ai3.supported((1, 8, 16, 16), 8, 3, padding=1, algorithm=name), name
+    assert not ai3.supported((1, 8, 16, 16), 8, 3, groups=2, algorithm="implicit_precomp_gemm")
 
 
 def _all_problem_shapes():

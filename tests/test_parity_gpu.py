@@ -16,7 +16,7 @@ from synth import CONFIG1, ConvShape, integer_inputs
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ["direct", "gemm", "implicit_gemm", "winograd", "smm", "kn2row", "guess"]
+ALGOS = ["direct", "gemm", "implicit_gemm", "implicit_precomp_gemm", "winograd", "smm", "kn2row", "guess"]
 MODES = [("f32", "strict"), ("f32", "tf32"), ("bf16", "strict")]
 
 
@@ -79,7 +79,7 @@ def test_ragged_shapes(shape, algo, dtype, math):
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
-@pytest.mark.parametrize("algo", ["implicit_gemm", "gemm", "winograd", "direct", "smm", "kn2row"])
+@pytest.mark.parametrize("algo", ["implicit_gemm", "implicit_precomp_gemm", "gemm", "winograd", "direct", "smm", "kn2row"])
 def test_layouts_bf16(layout, algo):
     _check(RAGGED[0], algo, "bf16", "strict", layout, seed=7)
 
@@ -153,7 +153,7 @@ def test_degenerate(shape, algo):
 
 
 # ------------------------------------------------------------------ determinism / batch independence
-@pytest.mark.parametrize("algo", ["direct", "gemm", "implicit_gemm", "winograd", "smm", "kn2row"])
+@pytest.mark.parametrize("algo", ["direct", "gemm", "implicit_gemm", "implicit_precomp_gemm", "winograd", "smm", "kn2row"])
 def test_deterministic_and_batch_independent(algo):
     """Same plan + input -> identical bits; and image n's output does not depend on the
     batch it was computed in (pins that batch sharding across GPUs is exact)."""
