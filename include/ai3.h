@@ -318,7 +318,8 @@ ai3_status ai3_conv2d_custom(const char* name, const ai3_tensor4d* x, const ai3_
  * given layouts; y is overwritten.  scratch: device, 256-byte aligned; algorithms whose
  * prepared weights + workspace exceed scratch_bytes are skipped (size it with
  * ai3_conv2d_autotune_scratch_bytes to run all).  The winner is cached per (problem,
- * dtype, math, layouts); AI3_ALGO_BENCHMARK then resolves to it everywhere. */
+ * dtype, math) -- the layouts it was measured in stand for all; AI3_ALGO_BENCHMARK then
+ * resolves to it everywhere. */
 ai3_status ai3_conv2d_autotune_scratch_bytes(const ai3_conv2d_params* params, const int64_t in_shape[4],
                                              ai3_dtype dtype, ai3_math math, int32_t in_layout,
                                              int32_t out_layout, size_t* bytes);

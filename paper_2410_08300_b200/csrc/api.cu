@@ -831,7 +831,7 @@ ai3_status ai3_conv2d_plan_create(const ai3_conv2d_params* params, const int64_t
     pl->wbuf = reinterpret_cast<char*>(weight_buf);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if ((s = prepare_weights(*pl, w, bias, st)) != AI3_OK) { delete pl; return s; }
-    if (r != AI3_ALGO_DIRECT && (s = encode_b_maps(*pl)) != AI3_OK) { delete pl; return s; }
+    if (r != AI3_ALGO_DIRECT && r != AI3_ALGO_SMM && (s = encode_b_maps(*pl)) != AI3_OK) { delete pl; return s; }
     *out = pl;
     return ok();
 }

@@ -5,7 +5,7 @@
 // :190/:200 contrast cuDNN's shape heuristic "guess" with measuring).
 //
 // Host logic over the public plan API; the timed work is the algorithms' own kernels.
-// The result is cached process-wide per (problem, dtype, math, layouts); afterwards the
+// The result is cached process-wide per (problem, dtype, math); afterwards the
 // algorithm id AI3_ALGO_BENCHMARK resolves to the cached winner (before that, to the
 // `guess` rule), so plans created with "benchmark" after one autotune call run the winner.
 #include <algorithm>
@@ -21,12 +21,14 @@ namespace {
 std::mutex g_tune_mu;
 std::map<std::string, ai3_algo> g_tuned;
 
-std::string make_key(const ai3_conv2d_params* p, const int64_t in[4], int dtype, int math, int inl, int outl) {
+// Keyed on the problem, dtype and math -- not on the layouts, which plan_weight_bytes does
+// not take: the winner measured in the caller's layouts stands for the problem.
+std::string make_key(const ai3_conv2d_params* p, const int64_t in[4], int dtype, int math) {
     char buf[320];
-    std::snprintf(buf, sizeof buf, "%lld,%lld,%lld,%lld|%lld,%d,%d|%d,%d|%d,%d|%d,%d|%d|%d|%d,%d|%d,%d",
+    std::snprintf(buf, sizeof buf, "%lld,%lld,%lld,%lld|%lld,%d,%d|%d,%d|%d,%d|%d,%d|%d|%d|%d,%d",
                   (long long)in[0], (long long)in[1], (long long)in[2], (long long)in[3], (long long)p->out_channels,
                   p->kernel[0], p->kernel[1], p->stride[0], p->stride[1], p->padding[0], p->padding[1],
-                  p->dilation[0], p->dilation[1], p->groups, p->has_bias, dtype, math, inl, outl);
+                  p->dilation[0], p->dilation[1], p->groups, p->has_bias, dtype, math);
     return buf;
 }
 }  // namespace
@@ -41,7 +43,7 @@ bool autotune_lookup(const ConvProblem& c, ai3_algo* out) {
     p.groups = c.G;
     p.has_bias = c.has_bias ? 1 : 0;
     const int64_t in[4] = {c.N, c.C, c.H, c.W};
-    const std::string k = make_key(&p, in, c.dtype, c.math, c.in_layout, c.out_layout);
+    const std::string k = make_key(&p, in, c.dtype, c.math);
     std::lock_guard<std::mutex> lk(g_tune_mu);
     auto it = g_tuned.find(k);
     if (it == g_tuned.end()) return false;
@@ -140,7 +142,7 @@ ai3_status ai3_conv2d_autotune(const ai3_conv2d_params* params, const int64_t in
     if (!found) return err != AI3_OK ? err : api_fail(AI3_ERR_WORKSPACE, "autotune: no algorithm fit the scratch buffer");
     {
         std::lock_guard<std::mutex> lk(g_tune_mu);
-        g_tuned[make_key(params, in_shape, dtype, math, in_layout, out_layout)] = *best;
+        g_tuned[make_key(params, in_shape, dtype, math)] = *best;
     }
     return AI3_OK;
 }

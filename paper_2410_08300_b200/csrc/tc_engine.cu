@@ -546,12 +546,15 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
+        // 32-column chunks holding real output channels (the last N tile may be partial: its
+        // padding columns are never read, and the TMEM release follows the last real chunk)
+        const int nvalid = min(ncol32, (a.Ncols - n0 + 31) / 32);
         uint32_t va[32], vb[32];
         tmem_ld32(tbase, va);
-        for (int c32 = 0; c32 < ncol32; c32 += 2) {
+        for (int c32 = 0; c32 < nvalid; c32 += 2) {
             // ---- chunk c32 (even): TMEM -> regs, prefetch c32+1
             tmem_ld_wait();
-            const bool has_b = c32 + 1 < ncol32;
+            const bool has_b = c32 + 1 < nvalid;
             if (has_b) tmem_ld32(tbase + (c32 + 1) * 32, vb);
             else {
                 tc_fence_before();
@@ -566,7 +569,7 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 if (hh == 1) {
                     if (!has_b) break;
                     tmem_ld_wait();
-                    if (c32 + 2 < ncol32) tmem_ld32(tbase + (c32 + 2) * 32, va);
+                    if (c32 + 2 < nvalid) tmem_ld32(tbase + (c32 + 2) * 32, va);
                     else {
                         tc_fence_before();
                         __syncwarp();
@@ -578,7 +581,6 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 }
                 const uint32_t* v = hh == 0 ? va : vb;
                 const int col0 = n0 + (c32 + hh) * 32;
-                if (col0 >= a.Ncols) break;
                 float f[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
@@ -721,6 +723,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ------------------------------------------------------------ epilogue (warps 2..5)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int group = (warp - 2) >> 2;  // epilogue warpgroup: takes every other tile
+        const bool single_group = (a.n_acc % (2 * ((a.num_kb + (a.promote_kb > 0 ? a.promote_kb : a.num_kb) - 1) /
+                                                   (a.promote_kb > 0 ? a.promote_kb : a.num_kb)))) != 0;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         const int nchunks = (a.num_kb + pk - 1) / pk;
@@ -866,7 +870,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int it = -1;  // index of the tile within this CTA group's sequence
         for (int tile = fast ? total_tiles : unit; tile < total_tiles; tile += num_units) {
             ++it;
-            if ((it & 1) != group) continue;
+            // Two warpgroups take alternate tiles only when each keeps to its own accumulator
+            // buffers (n_acc a multiple of 2 x chunks per tile): mbarrier parity waits cannot
+            // tell phase k from k+2, so two consumers of one buffer would race.
+            if (single_group ? group != 0 : (it & 1) != group) continue;
             {
                 const int chunk0 = it * nchunks;  // accumulation chunks before this tile
                 acc = chunk0 % a.n_acc;
@@ -995,10 +1002,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups) {
     // time ~ waves x per-tile cost; per-tile cost ~ max(BLOCK_N, 96) (MMA) + 48 (A-tile load and
     // epilogue overheads that do not shrink with BLOCK_N).  Partial last waves count in full.
-    const int cands[4] = {32, 64, 128, 256};
+    const int cands[5] = {32, 64, 128, 192, 256};  // 192: K = 192 / 384 layers (AlexNet) without padding
     int best = 32;
     long long best_cost = -1;
     for (int bn : cands) {
+        if (bn == 192 && Ncols % 192 != 0) continue;
         const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
         const long long waves = (units + num_groups - 1) / num_groups;
         const long long cost = waves * ((bn > 96 ? bn : 96) + 48);
@@ -1091,8 +1099,14 @@ void tc_configure(TcPlan& p, int num_sms) {
     p.smem_bytes = stages * stage_bytes + reserve;
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
-    a.n_acc = a.cm == CM_3XTF32 ? 2 : 512 / a.block_n;
+    a.n_acc = 512 / a.block_n;
     if (a.n_acc > MAX_ACC) a.n_acc = MAX_ACC;
+    if (a.cm == CM_3XTF32) {
+        // 3xTF32: `nch` accumulation chunks per tile; 2 x nch buffers let the two epilogue
+        // warpgroups alternate tiles on disjoint buffers, else one warpgroup drains them all
+        const int nch = (a.num_kb + a.promote_kb - 1) / a.promote_kb;
+        a.n_acc = 2 * nch <= a.n_acc ? 2 * nch : 2;
+    }
     if (a.n_acc < 2) a.n_acc = 2;
     int cols = 32;
     while (cols < a.n_acc * a.block_n) cols *= 2;

@@ -28,7 +28,7 @@ def _dev(a, dtype, nhwc=False):
 
 
 def _host(t):
-    return t.float().cpu().numpy().astype(np.float64)
+    return t.detach().float().cpu().numpy().astype(np.float64)
 
 
 def _rel(a, b):
