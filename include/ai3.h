@@ -204,6 +204,19 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
                                         void* x_dev, void* y_dev,
                                         void* workspace, size_t workspace_bytes, void* stream);
 
+/* A sequence of n independent executions from and to HOST memory, pipelined: every
+ * x_hosts[i] -> x_devs[i] copy is enqueued at once on an internal H2D copy stream, problem
+ * i computes on `stream` as soon as its input has landed, and y_devs[i] -> y_hosts[i]
+ * leaves on an internal D2H copy stream while problem i+1 computes -- the copy engines
+ * run both directions concurrently with the SMs.  Every x_devs[i] / y_devs[i] must be a
+ * distinct buffer; all problems share `workspace` (>= the largest plan's workspace size,
+ * used by one problem at a time on `stream`).  Work starts after what is already queued
+ * on `stream`, and `stream` is made to wait for the last copy: synchronise `stream`
+ * before reading any y_hosts[i].  Host buffers should be pinned. */
+ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, const void* const* x_hosts,
+                                         void* const* y_hosts, void* const* x_devs, void* const* y_devs,
+                                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Free the plan's host-side state (never the caller's device buffers). NULL is a no-op. */
 void ai3_conv2d_plan_destroy(ai3_plan* plan);
 

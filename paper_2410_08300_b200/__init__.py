@@ -15,11 +15,12 @@ provides device memory, streams and the module objects.
 """
 from ._lib import Ai3LibraryMissing, LIB_PATH
 from .conv import (ALGORITHMS, Ai3Error, ConvPlan, UnknownAlgorithm, UnsupportedConfiguration, algo_id, algo_name, autotune,
+                   execute_host_many,
                    check_supported, conv2d, guess, output_shape, supported)
 from .custom import register_conv2d, registered_count, unregister_conv2d
 from .hooks import Conv2D, Model, swap_backend, swap_conv2d
 
-__all__ = ["ALGORITHMS", "Ai3Error", "Ai3LibraryMissing", "autotune", "Conv2D", "ConvPlan", "LIB_PATH", "Model",
+__all__ = ["ALGORITHMS", "Ai3Error", "Ai3LibraryMissing", "autotune", "execute_host_many", "Conv2D", "ConvPlan", "LIB_PATH", "Model",
            "UnknownAlgorithm", "UnsupportedConfiguration", "algo_id", "algo_name", "check_supported", "conv2d",
            "guess", "output_shape", "register_conv2d", "registered_count", "supported", "swap_backend", "swap_conv2d",
            "unregister_conv2d", "version"]

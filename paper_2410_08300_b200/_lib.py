@@ -36,7 +36,7 @@ EXPORTS = ["ai3_version", "ai3_last_error", "ai3_algo_name", "ai3_algo_from_name
            "ai3_conv2d_plan_set_relu", "ai3_linear_plan_weight_bytes", "ai3_linear_plan_create", "ai3_relu",
            "ai3_pool2d_output_shape", "ai3_maxpool2d", "ai3_avgpool2d", "ai3_adaptive_avgpool2d",
            "ai3_layout_copy", "ai3_conv2d_autotune_scratch_bytes", "ai3_conv2d_autotune",
-           "ai3_conv2d_autotune_clear"]
+           "ai3_conv2d_autotune_clear", "ai3_conv2d_plans_execute_host"]
 
 
 class Ai3LibraryMissing(RuntimeError):
@@ -129,6 +129,8 @@ def load():
         "ai3_conv2d_autotune": ([pp, i64x4, ctypes.c_int, ctypes.c_int, i32, i32, vp, vp, vp, vp, vp, sz, i32, vp,
                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
         "ai3_conv2d_autotune_clear": ([], None),
+        "ai3_conv2d_plans_execute_host": ([i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                           ctypes.POINTER(vp), ctypes.POINTER(vp), vp, sz, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

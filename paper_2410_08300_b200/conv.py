@@ -263,6 +263,27 @@ def autotune(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = 
     return algo_name(best.value), {algo_name(i): float(ms[i]) for i in range(_lib.NUM_ALGOS) if ms[i] >= 0}
 
 
+def execute_host_many(plans, x_hosts, y_hosts, x_devs, y_devs):
+    """Pipelined host-to-host execution of independent problems (ai3_conv2d_plans_execute_host):
+    H2D copies, convolutions and D2H copies of consecutive problems overlap.  All buffers
+    are torch tensors (hosts pinned, devices distinct); synchronise the current stream
+    before reading the y_hosts."""
+    n = len(plans)
+    if not (len(x_hosts) == len(y_hosts) == len(x_devs) == len(y_devs) == n):
+        raise ValueError("one buffer of each kind per plan")
+    if n == 0:
+        return
+    dev = plans[0].device
+    ws = _WS.get(dev, max(p.workspace_size for p in plans))
+    arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])  # noqa: E731
+    hp = (ctypes.c_void_p * n)(*[p._h.value for p in plans])
+    _check(_lib.load().ai3_conv2d_plans_execute_host(n, hp, arr(x_hosts), arr(y_hosts), arr(x_devs), arr(y_devs),
+                                                     None if ws is None else ws.data_ptr(),
+                                                     0 if ws is None else ws.numel(), _stream_ptr(dev)))
+    for p in plans:
+        p._keep = None
+
+
 class ConvPlan:
     """Weights prepared once (swap time) for one input shape / layout / dtype.
 

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 #include <cstdarg>
 #include "internal.h"
 
@@ -859,6 +860,61 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
     if (s != AI3_OK) return s;
     e = cudaMemcpyAsync(y_host, y_dev, act_bytes(plan->pb, true), cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy of y");
+    return ok();
+}
+
+ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, const void* const* x_hosts,
+                                         void* const* y_hosts, void* const* x_devs, void* const* y_devs,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+    if (n < 0 || (n > 0 && (!plans || !x_hosts || !y_hosts || !x_devs || !y_devs)))
+        return fail(AI3_ERR_INVALID_ARGUMENT, "null plan / buffer array");
+    for (int32_t i = 0; i < n; ++i)
+        if (!plans[i] || !x_hosts[i] || !y_hosts[i] || !x_devs[i] || !y_devs[i])
+            return fail(AI3_ERR_INVALID_ARGUMENT, "null plan or buffer at index %d", (int)i);
+    if (n == 0) return ok();
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // one H2D and one D2H copy stream per device, created once (copy engines run both
+    // directions concurrently with the SMs)
+    static std::mutex smu;
+    static cudaStream_t cs[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return fail(AI3_ERR_CUDA, "device index out of range");
+    {
+        std::lock_guard<std::mutex> lk(smu);
+        for (int k = 0; k < 2; ++k)
+            if (!cs[dev][k] && cudaStreamCreateWithFlags(&cs[dev][k], cudaStreamNonBlocking) != cudaSuccess)
+                return fail(AI3_ERR_CUDA, "copy stream creation failed");
+    }
+    cudaStream_t h2d = cs[dev][0], d2h = cs[dev][1];
+    std::vector<cudaEvent_t> ev(2 * (size_t)n + 2);
+    for (auto& e : ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return fail(AI3_ERR_CUDA, "event creation failed");
+    cudaEvent_t start = ev[2 * n], done = ev[2 * n + 1];
+    ai3_status s = AI3_OK;
+    cudaError_t e = cudaEventRecord(start, st);  // copies begin after the caller's prior work
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, start, 0);
+    for (int32_t i = 0; i < n && e == cudaSuccess; ++i) {  // all inputs stream in back to back
+        e = cudaMemcpyAsync(x_devs[i], x_hosts[i], act_bytes(plans[i]->pb, false), cudaMemcpyHostToDevice, h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * i], h2d);
+    }
+    for (int32_t i = 0; i < n && e == cudaSuccess && s == AI3_OK; ++i) {
+        e = cudaStreamWaitEvent(st, ev[2 * i], 0);  // problem i computes once its input landed
+        if (e != cudaSuccess) break;
+        s = execute(*plans[i], x_devs[i], y_devs[i], workspace, workspace_bytes, st);
+        if (s != AI3_OK) break;
+        e = cudaEventRecord(ev[2 * i + 1], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev[2 * i + 1], 0);  // ...and leaves while i+1 computes
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(y_hosts[i], y_devs[i], act_bytes(plans[i]->pb, true), cudaMemcpyDeviceToHost, d2h);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(done, d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, done, 0);  // join: `stream` covers every copy
+    for (auto& x : ev) cudaEventDestroy(x);
+    if (s != AI3_OK) return s;
+    if (e != cudaSuccess) return cuda_fail(e, "pipelined host execution");
     return ok();
 }
 

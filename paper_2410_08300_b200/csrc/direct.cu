@@ -4,8 +4,9 @@
 // CUDA-core FFMA with fp32 accumulation; bound by the FP32 pipe (VGG/ResNet
 // layers have >= 16 flop/byte against an 11.5 flop/byte FFMA ridge).
 //
-// One CTA (256 threads, 8 warps) computes 32 output channels x (8 rows x 64 columns)
-// output pixels of one image / group.  Per chunk of CB input channels the CTA stages the
+// One CTA (256 threads, 8 warps) computes 32 output channels x 64*8 output pixels (8 x 64,
+// 16 x 32 or 32 x 16 rows x columns, whichever pads the layer's P x Q least) of one image /
+// group.  Per chunk of CB input channels the CTA stages the
 // zero-padded input footprint and the chunk's weights ([cc][r][s][32 k], k fastest) in
 // shared memory.  Each thread owns an 8-channel x 8-pixel register tile (one output row,
 // 8 consecutive columns; 64 fp32 accumulators).  Per (channel, filter row) it reads its
@@ -16,11 +17,12 @@
 // Handles any stride / padding / dilation / groups and NCHW or NHWC, fp32 or bf16.
 #include <cuda_bf16.h>
 #include "internal.h"
+#include "stage.cuh"
 
 namespace ai3 {
 
 namespace {
-constexpr int TK = 32, TP = 8, TQ = 64, NT = 256, VQ = 8;
+constexpr int TK = 32, NT = 256, VQ = 8;
 
 __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
@@ -29,14 +31,17 @@ __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
 
 // KS: compile-time square kernel size (0 = runtime R, S).  UNIT: stride 1 and dilation 1
 // along w (the row segment is loaded with 128-bit loads and slid in registers).
-template <int KS, bool UNIT>
+// QG: column groups of 8 pixels per tile row (tile = (64 / QG) rows x 8*QG columns), picked
+// per layer so that small feature maps (28x28, 14x14) do not pad to 64-wide tiles.
+template <int KS, bool UNIT, int QG>
 __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
                                                             int xs_floats) {
+    constexpr int TQ = VQ * QG, TP = 64 / QG;
     extern __shared__ __align__(16) float smem[];
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
     const int tid = threadIdx.x;
-    const int qg = tid & 7, pr = (tid >> 3) & 7, kg = tid >> 6;  // a warp: one k group, 4 rows x 8 column groups
+    const int qg = tid % QG, pr = (tid & 63) / QG, kg = tid >> 6;  // a warp: one k group (broadcast weights)
     const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
     const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
     const int k0g = blockIdx.y * TK;
@@ -61,23 +66,21 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     for (int c0 = 0; c0 < a.Cg; c0 += CB) {
         const int cb = min(CB, a.Cg - c0);
         // ---- stage the input footprint (zeros outside the image)
-        const int nx = cb * FH * FW;
-        for (int idx = tid; idx < nx; idx += NT) {
-            int cc, y, xw;
-            if (a.in_nhwc) { cc = idx % cb; const int t = idx / cb; xw = t % FW; y = t / FW; }
-            else { xw = idx % FW; const int t = idx / FW; y = t % FH; cc = t / FH; }
-            const int ih = ih0 + y, iw = iw0 + xw;
-            float v = 0.f;
-            if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
-                v = ldx(a.x, xbase + (int64_t)(c0 + cc) * xsC + (int64_t)ih * xsH + (int64_t)iw * xsW, a.bf16);
-            xs[(cc * FH + y) * FWp + xw] = v;
-        }
+        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
+                            ih0, iw0, cb, FH, FW, FWp, tid);
         // ---- stage weights [cc][r][s][TK] (contiguous rows of the prepared layout)
         const int nw = cb * R * S * TK;
-        for (int idx = tid; idx < nw; idx += NT) {
-            const int kk = idx % TK;
-            const int t = idx / TK;  // (cc, r, s)
-            ws[idx] = a.w[((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S + t) * a.Kgp + k0g + kk];
+        const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+        for (int base = 0; base < nw; base += NT * 4) {  // 4 loads in flight per thread
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int idx = base + u * NT + tid;
+                v[u] = idx < nw ? wsrc[(int64_t)(idx / TK) * a.Kgp + idx % TK] : 0.f;  // row (cc, r, s), column k
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (base + u * NT + tid < nw) ws[base + u * NT + tid] = v[u];
         }
         __syncthreads();
         for (int cc = 0; cc < cb; ++cc) {
@@ -149,12 +152,13 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     }
 }
 
-cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
+template <int QG>
+static cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
+    constexpr int TQ = VQ * QG, TP = 64 / QG;
     const bool unit = a.sw == 1 && a.dw == 1;
     const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
-    // 16-byte aligned rows; unit-stride segments may read up to 3 floats past FW (zeroed
-    // region never used for the result: loads beyond VQ + S - 1 are discarded)
+    // 16-byte aligned rows; unit-stride row segments read up to 3 floats past FW (never used)
     int FWp = (FW + 3 + 3) / 4 * 4;
     if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
     const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
@@ -174,19 +178,31 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
     };
     const bool sq = a.R == a.S;
     if (unit) {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, true>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true>);
-        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true>);
-        else if (sq && a.R == 7) launch(direct_conv_kernel<7, true>);
-        else launch(direct_conv_kernel<0, true>);
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG>);
+        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG>);
+        else launch(direct_conv_kernel<0, true, QG>);
     } else {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, false>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false>);
-        else if (sq && a.R == 7) launch(direct_conv_kernel<7, false>);
-        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false>);
-        else launch(direct_conv_kernel<0, false>);
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG>);
+        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG>);
+        else launch(direct_conv_kernel<0, false, QG>);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
+    // tile shape with the least padded area (ties: the widest rows)
+    int best = 8;
+    long long best_area = -1;
+    for (int qg : {8, 4, 2}) {
+        const long long tq = 8 * qg, tp = 64 / qg;
+        const long long area = ((a.P + tp - 1) / tp) * tp * ((a.Q + tq - 1) / tq) * tq;
+        if (best_area < 0 || area < best_area) { best = qg; best_area = area; }
+    }
+    if (best == 8) return launch_direct_qg<8>(a, st);
+    if (best == 4) return launch_direct_qg<4>(a, st);
+    return launch_direct_qg<2>(a, st);
 }
 
 }  // namespace ai3

@@ -19,6 +19,7 @@
 // Any stride / padding / dilation / groups, NCHW or NHWC in and out, fp32 or bf16.
 #include <cuda_bf16.h>
 #include "internal.h"
+#include "stage.cuh"
 
 namespace ai3 {
 
@@ -63,23 +64,21 @@ __global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB
     for (int c0 = 0; c0 < a.Cg; c0 += PB) {
         const int pb = min(PB, a.Cg - c0);
         // ---- zero-packed planes of channels c0 .. c0+pb-1 (padding written as zeros)
-        const int nx = pb * FH * FW;
-        for (int idx = tid; idx < nx; idx += NT) {
-            int cc, y, xw;
-            if (a.in_nhwc) { cc = idx % pb; const int t = idx / pb; xw = t % FW; y = t / FW; }
-            else { xw = idx % FW; const int t = idx / FW; y = t % FH; cc = t / FH; }
-            const int ih = ih0 + y, iw = iw0 + xw;
-            float v = 0.f;
-            if (ih >= 0 && ih < a.H && iw >= 0 && iw < a.W)
-                v = ld_act(a.x, xbase + (int64_t)(c0 + cc) * xsC + (int64_t)ih * xsH + (int64_t)iw * xsW, a.bf16);
-            xs[cc * plane + y * FWp + xw] = v;
-        }
+        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
+                            ih0, iw0, pb, FH, FW, FWp, tid);
         // ---- the scalars: w[k0g .. k0g+KT)[c][r][s]
         const int nw = pb * R * S * KT;
-        for (int idx = tid; idx < nw; idx += NT) {
-            const int kk = idx % KT;
-            const int t = idx / KT;  // (cc, r, s)
-            wsm[idx] = a.w[((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S + t) * a.Kgp + k0g + kk];
+        const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+        for (int base = 0; base < nw; base += NT * 4) {  // 4 loads in flight per thread
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int idx = base + u * NT + tid;
+                v[u] = idx < nw ? wsrc[(int64_t)(idx / KT) * a.Kgp + idx % KT] : 0.f;  // row (cc, r, s), column k
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (base + u * NT + tid < nw) wsm[base + u * NT + tid] = v[u];
         }
         __syncthreads();
         for (int cc = 0; cc < pb; ++cc) {

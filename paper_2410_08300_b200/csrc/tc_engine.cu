@@ -227,12 +227,25 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
     const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = unit; tile < tiles_per_batch; tile += num_units) {
+    const int taps = a.num_kb / a.c_chunks;
+    // the 4 table entries of this lane for (tile, tap); loaded one tap ahead of use so the
+    // global-load latency hides behind the previous tap's stage waits
+    auto rows_of = [&](int tile, int tap) -> int4 {
         const int mt = tile / a.n_tiles;
         const int m0 = mt * (BM * CG) + (int)rank * BM;
+        return *reinterpret_cast<const int4*>(a.gather_idx + (size_t)tap * a.gather_rows + m0 + 4 * lane);
+    };
+    int4 r_cur = unit < tiles_per_batch ? rows_of(unit, 0) : make_int4(-1, -1, -1, -1);
+    for (int tile = unit; tile < tiles_per_batch; tile += num_units) {
+        const int mt = tile / a.n_tiles;
         const int n0 = (tile - mt * a.n_tiles) * a.block_n + (int)rank * bn_cta;
         int cc = 0, tap = 0;
+        int4 r_next = r_cur;
         for (int kb = 0; kb < a.num_kb; ++kb) {
+            if (cc == 0) {  // prefetch the next tap's rows (or the next tile's first tap)
+                if (tap + 1 < taps) r_next = rows_of(tile, tap + 1);
+                else if (tile + num_units < tiles_per_batch) r_next = rows_of(tile + num_units, 0);
+            }
             if (lane == 0) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (CG == 1) mbar_arrive_expect_tx(&full[stage], stage_bytes);
@@ -241,7 +254,7 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
             __syncwarp();
             uint8_t* sA = smem + stage * stage_bytes;
             uint8_t* sB = sA + splits * a_bytes;
-            const int4 r = *reinterpret_cast<const int4*>(a.gather_idx + (size_t)tap * a.gather_rows + m0 + 4 * lane);
+            const int4 r = r_cur;
             const int cx = cc * kelems;
             uint8_t* dA = sA + lane * 4 * a.row_bytes;
             if (CG == 1) {
@@ -260,7 +273,7 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
                     if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kb * kelems, n0);
                 }
             }
-            if (++cc == a.c_chunks) { cc = 0; ++tap; }
+            if (++cc == a.c_chunks) { cc = 0; ++tap; r_cur = r_next; }
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
         }
     }

@@ -191,3 +191,36 @@ def test_errors_surface_as_exceptions():
         ai3.conv2d(x, w, None, 1, 0, 1, 1, "nope")
     with pytest.raises(ai3.Ai3Error):
         ai3.conv2d(x, torch.zeros(4, 3, 9, 9, device="cuda"), None)  # kernel larger than input
+
+
+# ------------------------------------------------------------------ host-to-host execution (bench e2e path)
+def test_execute_host_single_and_pipelined_match_device():
+    """ai3_conv2d_plan_execute_host and the pipelined ai3_conv2d_plans_execute_host give the
+    device path's bits, and the device result matches the oracle."""
+    import paper_2410_08300_b200 as ai3
+    shapes = [ConvShape("h0", 3, 64, 20, 20, 64, 3, 3, 1, 1), ConvShape("h1", 2, 32, 17, 15, 48, 1, 1),
+              ConvShape("h2", 1, 3, 33, 33, 16, 3, 3, 2, 1)]
+    plans, xh, yh, xd, yd, want = [], [], [], [], [], []
+    for i, sh in enumerate(shapes):
+        x, w, b = inputs(sh, 40 + i, "bf16")
+        xt = to_device(x, "bf16", "nhwc")
+        p = ai3.ConvPlan(to_device(w, "bf16"), to_device(b, "bf16"), xt.shape, sh.stride, sh.pad, sh.dil, 1,
+                         "guess", in_layout=1)
+        y = p(xt)
+        r = oracle.conv2d(xt.float().cpu().numpy(), to_device(w, "bf16").float().cpu().numpy(),
+                          to_device(b, "bf16").float().cpu().numpy(), sh.stride, sh.pad, sh.dil)
+        assert oracle.rel_err(y.float().cpu().numpy(), r) <= 2e-2
+        plans.append(p)
+        xh.append(xt.cpu().pin_memory())
+        yh.append(torch.empty_like(y, device="cpu").pin_memory())
+        xd.append(torch.empty_like(xt))
+        yd.append(torch.empty_like(y))
+        want.append(y.cpu())
+    ai3.execute_host_many(plans, xh, yh, xd, yd)
+    torch.cuda.synchronize()
+    for a, b_ in zip(yh, want):
+        assert torch.equal(a, b_)
+    y1 = torch.empty_like(yh[0]).pin_memory()
+    plans[0].execute_host(xh[0], y1, xd[0], yd[0])
+    torch.cuda.synchronize()
+    assert torch.equal(y1, want[0])
