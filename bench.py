@@ -293,6 +293,39 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "overlapped on copy streams), pinned host memory"}
         del hx, hy
 
+    # ---- the other BASELINE conv configs (ResNet-50 N=256, AlexNet N=128; bf16 NHWC, `guess`):
+    #      every unique layer shape timed once per rep, weighted by its count in the network
+    configs = None
+    if not args.no_configs and rank == 0:
+        configs = {}
+        for net, nb in (("resnet50", 256), ("alexnet", 128)):
+            try:
+                tot_ms, tot_flops, algos, launches = 0.0, 0, {}, 0
+                for i, spec in enumerate(workload(net, nb)):
+                    lay = Layer(spec, args.algo, device, seed=3000 + i)
+                    for _ in range(2):
+                        lay.run(stream.cuda_stream)
+                    reps = 10
+                    s1, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s1.record(stream)
+                    for _ in range(reps):
+                        lay.run(stream.cuda_stream)
+                    e1.record(stream)
+                    e1.synchronize()
+                    ms = s1.elapsed_time(e1) / reps
+                    tot_ms += spec.count * ms
+                    tot_flops += spec.count * spec.flops()
+                    launches += spec.count * lay.plan.num_launches
+                    algos[lay.plan.algorithm] = algos.get(lay.plan.algorithm, 0) + spec.count
+                    del lay
+                configs[net] = {"batch": nb, "convs": sum(sp.count for sp in workload(net, nb)),
+                                "ms_all_convs": round(tot_ms, 4), "tflops": round(tot_flops / (tot_ms * 1e-3) / 1e12, 1),
+                                "images_per_s": round(nb / (tot_ms * 1e-3), 1), "algorithms": algos,
+                                "launches": launches}
+                torch.cuda.empty_cache()
+            except Exception as ex:  # report, do not hide
+                configs[net] = {"error": str(ex)}
+
     # ---- the whole model: swap_backend(VGG-16), every op in ai3 (BASELINE configs[4]'s model
     #      at this rank's batch), timed the same way; reported beside the conv-stack metric
     model_leg = None
@@ -359,7 +392,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                            "l2": "step working set ~2.9 GB of distinct per-layer buffers >> 126 MB L2; no flush"},
                 "images_per_s": images_per_s, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "per_layer": per_layer,
-                "per_algorithm_tflops": per_algo, "vgg16_model": model_leg}
+                "per_algorithm_tflops": per_algo, "vgg16_model": model_leg, "other_configs": configs}
         print(json.dumps(line), flush=True)
 
 
@@ -374,6 +407,7 @@ def main():
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-model", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -267,7 +267,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     size_t off = 0;
     if (algo == AI3_ALGO_DIRECT || algo == AI3_ALGO_SMM) {
         const int64_t Kg = c.K / c.G, Cg = c.C / c.G;
-        pl.Kgp = round_up(Kg, 32);
+        pl.Kgp = round_up(Kg, 64);  // direct reads 64-channel k blocks, smm 16
         pl.w_off = 0;
         off = align_up((size_t)c.G * Cg * c.R * c.S * pl.Kgp * 4);
         pl.bias_off = off;

@@ -4,9 +4,9 @@
 // CUDA-core FFMA with fp32 accumulation; bound by the FP32 pipe (VGG/ResNet
 // layers have >= 16 flop/byte against an 11.5 flop/byte FFMA ridge).
 //
-// One CTA (256 threads, 8 warps) computes 32 output channels x 64*8 output pixels (8 x 64,
-// 16 x 32 or 32 x 16 rows x columns, whichever pads the layer's P x Q least) of one image /
-// group.  Per chunk of CB input channels the CTA stages the
+// One CTA (256 threads, 8 warps) computes 64 output channels x 256 output pixels (or 32 x
+// 512 for groups of <= 32 channels; 4 x 64 / 8 x 32 / 16 x 16 ... rows x columns, whichever
+// pads the layer's P x Q least) of one image / group.  Per chunk of CB input channels the CTA stages the
 // zero-padded input footprint and the chunk's weights ([cc][r][s][32 k], k fastest) in
 // shared memory.  Each thread owns an 8-channel x 8-pixel register tile (one output row,
 // 8 consecutive columns; 64 fp32 accumulators).  Per (channel, filter row) it reads its
@@ -22,7 +22,7 @@
 namespace ai3 {
 
 namespace {
-constexpr int TK = 32, NT = 256, VQ = 8;
+constexpr int NT = 256, VQ = 8;
 
 __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
@@ -31,17 +31,20 @@ __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
 
 // KS: compile-time square kernel size (0 = runtime R, S).  UNIT: stride 1 and dilation 1
 // along w (the row segment is loaded with 128-bit loads and slid in registers).
-// QG: column groups of 8 pixels per tile row (tile = (64 / QG) rows x 8*QG columns), picked
-// per layer so that small feature maps (28x28, 14x14) do not pad to 64-wide tiles.
-template <int KS, bool UNIT, int QG>
+// NKG: k groups of 8 output channels per CTA (TK = 8 * NKG; 8 = one warp per k group, so
+// every staged input element feeds 64 channels).  QG: column groups of 8 pixels per tile
+// row; the tile is (256 / NKG / QG) rows x 8*QG columns, picked per layer so that small
+// feature maps (28x28, 14x14) do not pad to 64-wide tiles.
+template <int KS, bool UNIT, int QG, int NKG>
 __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
                                                             int xs_floats) {
-    constexpr int TQ = VQ * QG, TP = 64 / QG;
+    constexpr int TK = 8 * NKG, PT = NT / NKG;  // pixel threads per k group
+    constexpr int TQ = VQ * QG, TP = PT / QG;
     extern __shared__ __align__(16) float smem[];
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
     const int tid = threadIdx.x;
-    const int qg = tid % QG, pr = (tid & 63) / QG, kg = tid >> 6;  // a warp: one k group (broadcast weights)
+    const int qg = tid % QG, pr = (tid % PT) / QG, kg = tid / PT;  // a warp: one k group (broadcast weights)
     const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
     const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
     const int k0g = blockIdx.y * TK;
@@ -152,9 +155,9 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     }
 }
 
-template <int QG>
+template <int QG, int NKG>
 static cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
-    constexpr int TQ = VQ * QG, TP = 64 / QG;
+    constexpr int TK = 8 * NKG, TQ = VQ * QG, TP = NT / NKG / QG;
     const bool unit = a.sw == 1 && a.dw == 1;
     const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
@@ -178,31 +181,39 @@ static cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     };
     const bool sq = a.R == a.S;
     if (unit) {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG>);
-        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG>);
-        else launch(direct_conv_kernel<0, true, QG>);
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG>);
+        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG, NKG>);
+        else launch(direct_conv_kernel<0, true, QG, NKG>);
     } else {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG>);
-        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG>);
-        else launch(direct_conv_kernel<0, false, QG>);
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG, NKG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG, NKG>);
+        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG, NKG>);
+        else launch(direct_conv_kernel<0, false, QG, NKG>);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
-    // tile shape with the least padded area (ties: the widest rows)
+    // 64 channels per CTA when the group has them (halves the staging per FFMA), else 32;
+    // then the tile shape with the least padded area (ties: the widest rows)
+    const int nkg = a.Kg > 32 ? 8 : 4;
+    const int pt = NT / nkg;
     int best = 8;
     long long best_area = -1;
     for (int qg : {8, 4, 2}) {
-        const long long tq = 8 * qg, tp = 64 / qg;
+        const long long tq = 8 * qg, tp = pt / qg;
         const long long area = ((a.P + tp - 1) / tp) * tp * ((a.Q + tq - 1) / tq) * tq;
         if (best_area < 0 || area < best_area) { best = qg; best_area = area; }
     }
-    if (best == 8) return launch_direct_qg<8>(a, st);
-    if (best == 4) return launch_direct_qg<4>(a, st);
-    return launch_direct_qg<2>(a, st);
+    if (nkg == 8) {
+        if (best == 8) return launch_direct_qg<8, 8>(a, st);
+        if (best == 4) return launch_direct_qg<4, 8>(a, st);
+        return launch_direct_qg<2, 8>(a, st);
+    }
+    if (best == 8) return launch_direct_qg<8, 4>(a, st);
+    if (best == 4) return launch_direct_qg<4, 4>(a, st);
+    return launch_direct_qg<2, 4>(a, st);
 }
 
 }  // namespace ai3

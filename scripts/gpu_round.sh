@@ -10,8 +10,8 @@ tail -3 gpurun_out/bench.err
 cat gpurun_out/bench.json
 if [ "${NCU:-1}" = "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-   python bench.py --steps 2 --warmup 3 --no-e2e --no-compare --no-cpu --no-model > /dev/null 2>&1; echo "ncu list rc=$?"
+   python bench.py --steps 2 --warmup 3 --no-e2e --no-compare --no-cpu --no-model --no-configs > /dev/null 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 16 -c 2 -o gpurun_out/prof_tc -f \
-   python bench.py --steps 1 --warmup 3 --no-e2e --no-compare --no-cpu --no-model > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+   python bench.py --steps 1 --warmup 3 --no-e2e --no-compare --no-cpu --no-model --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 tail -3 gpurun_out/ncu_full.log
 fi
