@@ -71,8 +71,8 @@ typedef enum {
     AI3_ALGO_GEMM = 2,              /* "gemm", "im2col" */
     AI3_ALGO_IMPLICIT_GEMM = 3,     /* "implicit_gemm" */
     AI3_ALGO_WINOGRAD = 4,          /* "winograd" */
-    /* SURVEY §8f rows; "implicit_precomp_gemm" is AI3_ERR_UNSUPPORTED until built */
-    AI3_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* "implicit_precomp_gemm" */
+    /* SURVEY §8f rows */
+    AI3_ALGO_IMPLICIT_PRECOMP_GEMM = 5, /* "implicit_precomp_gemm": implicit GEMM over a precomputed input-row table, TMA gather4 */
     AI3_ALGO_SMM = 6,               /* "smm": scalar matrix multiplication (§II.B(c)) */
     AI3_ALGO_KN2ROW = 7,            /* "kn2row": kernel-to-row 1x1 GEMMs + shift-accumulate (§II.B(b)) */
     AI3_ALGO_CUSTOM = 8,            /* "custom": the registered user algorithm (see below) */
