@@ -18,7 +18,12 @@
  *   AI3_ALGO_GEMM           -- explicit IM2COL matrix + GEMM (§II.B(a), :194 §V.B(c))
  *   AI3_ALGO_IMPLICIT_GEMM  -- GEMM without forming the matrix, zero extra memory (§V.B(b))
  *   AI3_ALGO_WINOGRAD       -- Winograd minimal filtering F(2x2,3x3) (§V.B(d))
+ *   AI3_ALGO_IMPLICIT_PRECOMP_GEMM -- implicit GEMM over a precomputed index table
+ *   AI3_ALGO_SMM            -- scalar matrix multiplication: shifted planes x scalar weights
+ *   AI3_ALGO_KN2ROW         -- kernel-to-row: R*S 1x1 GEMMs + shift-accumulate
  *   AI3_ALGO_GUESS          -- shape-based heuristic choice ("guess")
+ *   AI3_ALGO_BENCHMARK      -- the fastest algorithm measured by ai3_conv2d_autotune
+ *   AI3_ALGO_CUSTOM         -- a user-registered algorithm
  * All algorithms compute the same function; they differ in rounding only.
  *
  * Conventions (all entry points):
