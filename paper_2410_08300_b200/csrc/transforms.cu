@@ -223,14 +223,23 @@ cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t
 }
 
 // ---------------------------------------------------------------- Winograd input transform
-// One thread per (tile t, group of VC channels).  x is NHWC (Cpad), bf16 when
-// cm == CM_BF16 else fp32 (unrounded); V is written in compute-mode precision.
-template <int VC, bool BF16IN>
-__global__ void winograd_input_kernel(const void* __restrict__ xin, int64_t N, int64_t H, int64_t W, int64_t Cpad,
-                                      int64_t TH, int64_t TW, int ph, int pw, int cm, void* V, void* V_lo) {
+// One thread per (tile t, group of 4 channels).  x is NHWC (Cpad), bf16 when cm == CM_BF16
+// else fp32 (unrounded); V[xi*4+nu][t][c] is written in compute-mode precision with one
+// vector store per (xi, nu): 8 bytes (bf16) or 16 bytes (fp32; + the lo part for 3xTF32).
+// (B^T d B)[a][b] = sum_ij B^T[a][i] B^T[b][j] d[i][j]: every B^T row has two +-1 entries.
+__device__ __forceinline__ float bt_comb(const float (&r)[4], int a) {
+    return a == 0 ? r[0] - r[2] : (a == 1 ? r[1] + r[2] : (a == 2 ? r[2] - r[1] : r[1] - r[3]));
+}
+
+template <bool BF16IN>
+__global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restrict__ xin, int64_t N, int64_t H,
+                                                             int64_t W, int64_t Cpad, int64_t TH, int64_t TW, int ph,
+                                                             int pw, int cm, void* V, void* V_lo) {
+    constexpr int VC = 4;
     const int64_t groups = Cpad / VC;
     const int64_t T = N * TH * TW;
     const int64_t total = T * groups;
+    const int64_t plane = T * Cpad;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = i / groups, cgi = i % groups;
         const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
@@ -244,42 +253,51 @@ __global__ void winograd_input_kernel(const void* __restrict__ xin, int64_t N, i
                 const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
                 const int64_t off = ((n * H + ih) * W + iw) * Cpad + cgi * VC;
                 if (BF16IN) {
-                    uint4 raw = ok ? *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(xin) + off)
-                                   : make_uint4(0, 0, 0, 0);
+                    const uint2 raw = ok ? *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(xin) + off)
+                                         : make_uint2(0, 0);
                     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
                     for (int v = 0; v < VC; ++v) d[a][b][v] = __bfloat162float(e[v]);
                 } else {
-                    float4 raw = ok ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xin) + off)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const float* e = reinterpret_cast<const float*>(&raw);
-#pragma unroll
-                    for (int v = 0; v < VC; ++v) d[a][b][v] = e[v];
+                    const float4 raw = ok ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xin) + off)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                    d[a][b][0] = raw.x; d[a][b][1] = raw.y; d[a][b][2] = raw.z; d[a][b][3] = raw.w;
                 }
             }
         }
-        const int64_t plane = T * Cpad;
         const int64_t base = t * Cpad + cgi * VC;
 #pragma unroll
-        for (int v = 0; v < VC; ++v) {
-            float bt[4][4];  // B^T d
+        for (int a = 0; a < 4; ++a) {
+            float bt[4][VC];  // row a of B^T d, per channel
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+#pragma unroll
+                for (int v = 0; v < VC; ++v) {
+                    const float col[4] = {d[0][b][v], d[1][b][v], d[2][b][v], d[3][b][v]};
+                    bt[b][v] = bt_comb(col, a);
+                }
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                bt[0][b] = d[0][b][v] - d[2][b][v];
-                bt[1][b] = d[1][b][v] + d[2][b][v];
-                bt[2][b] = d[2][b][v] - d[1][b][v];
-                bt[3][b] = d[1][b][v] - d[3][b][v];
-            }
+                float o[VC];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {  // (B^T d) B
-                const float v0 = bt[a][0] - bt[a][2];
-                const float v1 = bt[a][1] + bt[a][2];
-                const float v2 = bt[a][2] - bt[a][1];
-                const float v3 = bt[a][1] - bt[a][3];
-                store_v(V, V_lo, (a * 4 + 0) * plane + base + v, v0, cm);
-                store_v(V, V_lo, (a * 4 + 1) * plane + base + v, v1, cm);
-                store_v(V, V_lo, (a * 4 + 2) * plane + base + v, v2, cm);
-                store_v(V, V_lo, (a * 4 + 3) * plane + base + v, v3, cm);
+                for (int v = 0; v < VC; ++v) {
+                    const float row[4] = {bt[0][v], bt[1][v], bt[2][v], bt[3][v]};
+                    o[v] = bt_comb(row, b);
+                }
+                const int64_t idx = (a * 4 + b) * plane + base;
+                if (cm == CM_BF16) {
+                    __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(o[0], o[1]), __floats2bfloat162_rn(o[2], o[3])};
+                    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(V) + idx) = *reinterpret_cast<const uint2*>(h);
+                } else if (cm == CM_TF32) {
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(V) + idx) =
+                        make_float4(tf32_round(o[0]), tf32_round(o[1]), tf32_round(o[2]), tf32_round(o[3]));
+                } else {
+                    float hi[VC], lo[VC];
+#pragma unroll
+                    for (int v = 0; v < VC; ++v) { hi[v] = tf32_round(o[v]); lo[v] = tf32_round(o[v] - hi[v]); }
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(V) + idx) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(V_lo) + idx) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                }
             }
         }
     }
@@ -289,20 +307,38 @@ cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W
                                   int64_t Q, int ph, int pw, ComputeMode cm, const void* /*x_lo*/, void* V,
                                   void* V_lo, cudaStream_t st) {
     const int64_t TH = (P + 1) / 2, TW = (Q + 1) / 2;
-    const int VC = cm == CM_BF16 ? 8 : 4;
-    const int64_t total = N * TH * TW * (Cpad / VC);
-    const int64_t blocks = (total + 127) / 128;
-    const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+    const int64_t total = N * TH * TW * (Cpad / 4);
+    const int64_t blocks = (total + 255) / 256;
+    const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
     if (cm == CM_BF16)
-        winograd_input_kernel<8, true><<<grid, 128, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+        winograd_input_kernel<true><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
     else
-        winograd_input_kernel<4, false><<<grid, 128, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+        winograd_input_kernel<false><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- Winograd output transform
 // M fp32: m_kt = 1 -> [16][K][T] (threads walk t fastest, NCHW stores coalesce);
-//         m_kt = 0 -> [16][T][K] (threads walk k fastest, NHWC stores coalesce).
+//         m_kt = 0 -> [16][T][K] (threads walk 4 channels at a time, NHWC: 16-byte M loads,
+//                   one 8-/16-byte store per output pixel).
+__device__ __forceinline__ void wino_out4(const float (&m)[4][4], float bv, int relu, float (&y)[2][2]) {
+    float at[2][4];  // A^T M
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        at[0][b] = m[0][b] + m[1][b] + m[2][b];
+        at[1][b] = m[1][b] - m[2][b] - m[3][b];
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {  // (A^T M) A
+        y[a][0] = at[a][0] + at[a][1] + at[a][2] + bv;
+        y[a][1] = at[a][1] - at[a][2] - at[a][3] + bv;
+        if (relu) {
+            y[a][0] = y[a][0] < 0.f ? 0.f : y[a][0];
+            y[a][1] = y[a][1] < 0.f ? 0.f : y[a][1];
+        }
+    }
+}
+
 __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, const float* __restrict__ bias, void* y,
                                        int out_nhwc, int bf16, int64_t N, int64_t K, int64_t P, int64_t Q,
                                        int64_t TH, int64_t TW, int relu) {
@@ -318,19 +354,8 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int b = 0; b < 4; ++b) m[a][b] = M[(a * 4 + b) * plane + off];
-        float at[2][4];  // A^T M
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            at[0][b] = m[0][b] + m[1][b] + m[2][b];
-            at[1][b] = m[1][b] - m[2][b] - m[3][b];
-        }
-        const float bv = bias ? bias[k] : 0.f;
         float yv[2][2];
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {  // (A^T M) A
-            yv[a][0] = at[a][0] + at[a][1] + at[a][2] + bv;
-            yv[a][1] = at[a][1] - at[a][2] - at[a][3] + bv;
-        }
+        wino_out4(m, bias ? bias[k] : 0.f, relu, yv);
         const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
@@ -341,9 +366,54 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
                 const int64_t q = 2 * tw + b;
                 if (q >= Q) break;
                 const int64_t o = out_nhwc ? ((n * P + p) * Q + q) * K + k : ((n * K + k) * P + p) * Q + q;
-                const float v = (relu && yv[a][b] < 0.f) ? 0.f : yv[a][b];
-                if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(v);
-                else reinterpret_cast<float*>(y)[o] = v;
+                if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(yv[a][b]);
+                else reinterpret_cast<float*>(y)[o] = yv[a][b];
+            }
+        }
+    }
+}
+
+// NHWC output, K % 4 == 0: one thread per (tile, 4 output channels).
+__global__ void __launch_bounds__(256) winograd_output_nhwc4_kernel(const float* __restrict__ M,
+                                                                    const float* __restrict__ bias, void* y, int bf16,
+                                                                    int64_t N, int64_t K, int64_t P, int64_t Q,
+                                                                    int64_t TH, int64_t TW, int relu) {
+    const int64_t T = N * TH * TW;
+    const int64_t kg = K / 4;
+    const int64_t total = T * kg;
+    const int64_t plane = T * K;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / kg, k0 = (i % kg) * 4;
+        const int64_t off = t * K + k0;
+        float4 mv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mv[j] = *reinterpret_cast<const float4*>(M + j * plane + off);
+        float out[4][2][2];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            float m[4][4];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) m[j / 4][j % 4] = v == 0 ? mv[j].x : (v == 1 ? mv[j].y : (v == 2 ? mv[j].z : mv[j].w));
+            wino_out4(m, bias ? bias[k0 + v] : 0.f, relu, out[v]);
+        }
+        const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const int64_t p = 2 * th + a;
+            if (p >= P) break;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int64_t q = 2 * tw + b;
+                if (q >= Q) break;
+                const int64_t o = ((n * P + p) * Q + q) * K + k0;
+                if (bf16) {
+                    __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(out[0][a][b], out[1][a][b]),
+                                                        __floats2bfloat162_rn(out[2][a][b], out[3][a][b])};
+                    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + o) = *reinterpret_cast<const uint2*>(h);
+                } else {
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + o) =
+                        make_float4(out[0][a][b], out[1][a][b], out[2][a][b], out[3][a][b]);
+                }
             }
         }
     }
@@ -352,6 +422,13 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
 cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
                                    int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st) {
     const int64_t TH = (P + 1) / 2, TW = (Q + 1) / 2;
+    if (!m_kt && out_nhwc && K % 4 == 0) {
+        const int64_t total = N * TH * TW * (K / 4);
+        const int64_t blocks = (total + 255) / 256;
+        const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+        winograd_output_nhwc4_kernel<<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
+        return cudaGetLastError();
+    }
     const int64_t total = N * TH * TW * K;
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
