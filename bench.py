@@ -172,7 +172,7 @@ class Layer:
         self.x = torch.randn((spec.N, spec.C, spec.H, spec.W), generator=g, device=device, dtype=torch.float32) \
             .to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
         wt = torch.from_numpy(w).to(device=device, dtype=torch.bfloat16)
-        bt = torch.from_numpy(b).to(device=device, dtype=torch.bfloat16)
+        bt = None if b is None else torch.from_numpy(b).to(device=device, dtype=torch.bfloat16)
         self.plan = ai3.ConvPlan(wt, bt, self.x.shape, spec.stride, spec.pad, spec.dil, spec.groups, algo,
                                  in_layout=1, out_layout=1)
         self.y = torch.empty(self.plan.out_shape, dtype=torch.bfloat16, device=device,

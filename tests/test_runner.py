@@ -66,3 +66,15 @@ def test_gloo_sharded_equals_unsharded(world, n):
     for rank, equal, t in res:
         assert equal, f"rank {rank}: gathered output differs from the unsharded run"
         assert t == float(world)  # max over ranks of (rank + 1)
+
+
+@pytest.mark.gpu
+def test_runner_single_gpu_all_ai3_vgg16():
+    """BASELINE configs[4] path on one GPU (world size 1): the all-ai3 VGG-16 forward over a
+    small global batch; sampled images run alone reproduce the batched logits bit for bit
+    (the property that makes batch sharding across GPUs exact)."""
+    pytest.importorskip("torchvision")
+    from paper_2410_08300_b200.runner import run
+    res = run(global_batch=6, algo="guess", steps=1, warmup=1, seed=123, check=True, swap="backend")
+    assert res["logits_bit_identical_when_sharded"], res
+    assert res["images_per_s"] > 0
