@@ -106,65 +106,76 @@ __global__ void im2col_kernel(const void* __restrict__ xin, int nhwc, int64_t N,
 }
 
 // Small-C variant (RGB first layers): one CTA per (image, band of TP output rows).  The
-// band's input footprint (all W columns, all C channels) is staged once in shared memory
-// (coalesced loads, rows outside the image zeroed), then the band's A rows are written
-// with 4-8 consecutive lanes covering one row (fully coalesced 16-byte stores).
-constexpr int IM2COL_TP = 2;
-
+// band's input footprint (FH rows x all W columns x C channels) is staged once in shared
+// memory with pw zero columns on each side and zero rows outside the image, so no element
+// needs a bounds test.  Every thread then owns one fixed 16-byte column group g of the A
+// row (its V band offsets and tail mask live in registers) and writes that group for
+// pixel after pixel: consecutive threads write consecutive 16-byte pieces of a row.
 template <bool BF16IN, int V>
 __global__ void __launch_bounds__(256) im2col_smallc_kernel(const void* __restrict__ xin, int nhwc, int C, int H,
                                                             int W, int P, int Q, int R, int S, int sh, int sw, int ph,
-                                                            int pw, int dh, int dw, int Kp, int FH, int cm, void* A,
-                                                            void* A_lo) {
-    extern __shared__ float band[];  // [FH][W][C]
+                                                            int pw, int dh, int dw, int Kp, int FH, int TPB, int cm,
+                                                            void* A, void* A_lo) {
+    extern __shared__ float band[];  // [FH][W + 2*pw][C], zero padded
     const int n = blockIdx.y;
-    const int p0 = blockIdx.x * IM2COL_TP;
+    const int p0 = blockIdx.x * TPB;
     const int ih0 = p0 * sh - ph;
-    const int nb = FH * W * C;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-        int y, xw, c;
-        if (nhwc) { c = i % C; const int t = i / C; xw = t % W; y = t / W; }
-        else { xw = i % W; const int t = i / W; y = t % FH; c = t / FH; }
-        const int ih = ih0 + y;
+    const int Wp = W + 2 * pw;
+    // band element coordinates advance by carries (no division per element): NHWC walks
+    // (c, xp, y), NCHW walks (xp, y, c) -- the contiguous axis of the input first
+    const int D0 = nhwc ? C : Wp, D1 = nhwc ? Wp : FH, D2 = nhwc ? FH : C;
+    const int NTB = blockDim.x;
+    const int s0 = NTB % D0, s1 = (NTB / D0) % D1, s2 = NTB / (D0 * D1);
+    int i0 = threadIdx.x % D0, i1 = (threadIdx.x / D0) % D1, i2 = threadIdx.x / (D0 * D1);
+    for (; i2 < D2;) {
+        const int c = nhwc ? i0 : i2, xp = nhwc ? i1 : i0, y = nhwc ? i2 : i1;
+        {
+            int cr = (i0 += s0) >= D0;
+            i0 -= cr ? D0 : 0;
+            i1 += s1 + cr;
+            cr = i1 >= D1;
+            i1 -= cr ? D1 : 0;
+            i2 += s2 + cr;
+        }
+        const int ih = ih0 + y, xw = xp - pw;
         float v = 0.f;
-        if (ih >= 0 && ih < H) {
+        if (ih >= 0 && ih < H && xw >= 0 && xw < W) {
             const int64_t off = nhwc ? (((int64_t)n * H + ih) * W + xw) * C + c : (((int64_t)n * C + c) * H + ih) * W + xw;
             v = BF16IN ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xin)[off])
                        : reinterpret_cast<const float*>(xin)[off];
         }
-        band[(y * W + xw) * C + c] = v;
+        band[(y * Wp + xp) * C + c] = v;
     }
     __syncthreads();
     const int groups = Kp / V;
     const int Kred = R * S * C;
-    const int rows = min(IM2COL_TP, P - p0) * Q;
-    // per-column gather table: band offset (relative to the window origin) and column shift
-    int* toff = reinterpret_cast<int*>(band + FH * W * C);
-    int* tsh = toff + Kp;
-    for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
+    const int rows = min(TPB, P - p0) * Q;
+    const int ppi = blockDim.x / groups;  // pixels per pass (>= 1: launch guarantees groups <= 256)
+    const int g = threadIdx.x % groups, slot = threadIdx.x / groups;
+    if (slot >= ppi) return;
+    int toff[V];
+    unsigned live = 0;  // columns of this group inside the exact reduction length R*S*C
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int kk = g * V + v;
+        toff[v] = 0;
         if (kk < Kred) {
             const int tap = kk / C, c = kk - tap * C;
             const int r = tap / S, sx = tap - r * S;
-            toff[kk] = (r * dh * W + sx * dw) * C + c;
-            tsh[kk] = sx * dw;
-        } else {
-            toff[kk] = 0;
-            tsh[kk] = -(1 << 28);  // always out of range -> 0
+            toff[v] = (r * dh * Wp + sx * dw) * C + c;
+            live |= 1u << v;
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < rows * groups; i += blockDim.x) {
-        const int pix = i / groups, g = i - pix * groups;
-        const int pl = pix / Q, q = pix - pl * Q;
-        const int iw0 = q * sw - pw;
-        const int org = (pl * sh * W + iw0) * C;  // band index of the window origin (may be negative)
+    int pl = slot / Q, q = slot - (slot / Q) * Q;  // (row, column) of pixel `pix`, advanced by carries
+    const int dpl = ppi / Q, dq = ppi - (ppi / Q) * Q;
+    for (int pix = slot; pix < rows; pix += ppi) {
+        const int org = (pl * sh * Wp + q * sw) * C;  // band index of the window origin (padded coords)
+        q += dq;
+        pl += dpl;
+        if (q >= Q) { q -= Q; ++pl; }
         float vals[V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const int kk = g * V + v;
-            const int iw = iw0 + tsh[kk];
-            vals[v] = (iw >= 0 && iw < W) ? band[org + toff[kk]] : 0.f;
-        }
+        for (int v = 0; v < V; ++v) vals[v] = (live >> v) & 1u ? band[org + toff[v]] : 0.f;
         const int64_t m = ((int64_t)n * P + p0) * Q + pix;
         const int64_t o = m * groups + g;
         if (cm == CM_BF16) {
@@ -192,15 +203,21 @@ cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t
                           ComputeMode cm, void* A, void* A_lo, cudaStream_t st) {
     {
         const int V = cm == CM_BF16 ? 8 : 4;
-        const int FH = (IM2COL_TP - 1) * sh + (R - 1) * dh + 1;
-        const size_t smem = (size_t)FH * W * C * sizeof(float) + 2 * (size_t)Kp * sizeof(int);
-        if (C * (dtype == AI3_BF16 ? 2 : 4) < 32 && smem <= 96 * 1024 && N <= 65535) {
-            dim3 grid((unsigned)((P + IM2COL_TP - 1) / IM2COL_TP), (unsigned)N);
+        // output rows per CTA: as many as fit 48 KB of band (fewer re-staged rows for large
+        // strides, while >= 4 CTAs stay resident per SM; measured: 96 KB bands were slower)
+        int TPB = 2;
+        while (TPB < 16 && TPB < P &&
+               (size_t)((TPB + 1) * sh + (R - 1) * dh + 1) * (W + 2 * pw) * C * sizeof(float) <= 48 * 1024)
+            ++TPB;
+        const int FH = (TPB - 1) * sh + (R - 1) * dh + 1;
+        const size_t smem = (size_t)FH * (W + 2 * pw) * C * sizeof(float);
+        if (C * (dtype == AI3_BF16 ? 2 : 4) < 32 && smem <= 96 * 1024 && N <= 65535 && Kp / V <= 256) {
+            dim3 grid((unsigned)((P + TPB - 1) / TPB), (unsigned)N);
             const int nhwc = in_layout == AI3_NHWC;
             auto go = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 kern<<<grid, 256, smem, st>>>(x, nhwc, (int)C, (int)H, (int)W, (int)P, (int)Q, R, S, sh, sw, ph, pw,
-                                              dh, dw, (int)Kp, FH, cm, A, A_lo);
+                                              dh, dw, (int)Kp, FH, TPB, cm, A, A_lo);
             };
             if (dtype == AI3_BF16) { if (V == 8) go(im2col_smallc_kernel<true, 8>); else go(im2col_smallc_kernel<true, 4>); }
             else { if (V == 8) go(im2col_smallc_kernel<false, 8>); else go(im2col_smallc_kernel<false, 4>); }
