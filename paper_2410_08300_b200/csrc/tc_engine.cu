@@ -1009,20 +1009,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // ---------------------------------------------------------------- host side
 
-// N tile: minimise n_tiles * max(BLOCK_N, 96) -- below ~96 columns an MMA is bound by
-// re-reading the 128-row A tile from shared memory, not by the tensor pipe.  Ties go to
-// the smaller tile (less padding, more CTAs).
-static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups) {
-    // time ~ waves x per-tile cost; per-tile cost ~ max(BLOCK_N, 96) (MMA) + 48 (A-tile load and
-    // epilogue overheads that do not shrink with BLOCK_N).  Partial last waves count in full.
+// N tile: the candidate with the least modelled time.  Per wave of concurrently running
+// tiles the time is the larger of
+//  * the tensor pipe: K-blocks x 32-byte K slices x cycles per MMA (measured tcgen05 rates,
+//    128xNx16 / 256xNx16 cost max(N/2, ~66 / ~46) cycles), and
+//  * the operand stream of that wave: every tile brings its A rows and its B slice through
+//    TMA from L2, at the chip's ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch
+//    runs at 11-12 TB/s of TMA loads),
+// plus a per-tile fill / drain.  Partial last waves count at their own size.
+static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups, int cg, int row_bytes, int num_kb) {
     const int cands[5] = {32, 64, 128, 192, 256};  // 192: K = 192 / 384 layers (AlexNet) without padding
+    const double kred_bytes = (double)row_bytes * num_kb;  // bytes of one operand row
     int best = 32;
-    long long best_cost = -1;
+    double best_cost = -1;
     for (int bn : cands) {
         if (bn == 192 && Ncols % 192 != 0) continue;
         const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
-        const long long waves = (units + num_groups - 1) / num_groups;
-        const long long cost = waves * ((bn > 96 ? bn : 96) + 48);
+        const long long full = units / num_groups, rest = units % num_groups;
+        const double mma_cyc = cg == 2 ? (bn >= 128 ? bn / 2.0 : 46.0) : (bn >= 128 ? bn / 2.0 : 66.5);
+        const double t_mma = (double)num_kb * (row_bytes / 32) * mma_cyc;
+        const double tile_bytes = (128.0 * cg + bn) * kred_bytes;
+        auto wave = [&](long long u) {
+            const double t_l2 = u * tile_bytes / 6300.0;
+            return (t_mma > t_l2 ? t_mma : t_l2) + 600.0;
+        };
+        const double cost = full * wave(num_groups) + (rest ? wave(rest) : 0.0);
         if (best_cost < 0 || cost < best_cost) { best = bn; best_cost = cost; }
     }
     return best;
@@ -1049,7 +1060,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.block_n == 0) {
         const int cg = pick_cg(a.M);
         const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
-        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg);
+        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb);
     }
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
     if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
