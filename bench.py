@@ -300,7 +300,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         configs = {}
         for net, nb in (("resnet50", 256), ("alexnet", 128)):
             try:
-                tot_ms, tot_flops, algos, launches = 0.0, 0, {}, 0
+                tot_ms, tot_flops, algos, launches, rows = 0.0, 0, {}, 0, []
                 for i, spec in enumerate(workload(net, nb)):
                     lay = Layer(spec, args.algo, device, seed=3000 + i)
                     for _ in range(2):
@@ -317,11 +317,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     tot_flops += spec.count * spec.flops()
                     launches += spec.count * lay.plan.num_launches
                     algos[lay.plan.algorithm] = algos.get(lay.plan.algorithm, 0) + spec.count
+                    rows.append([spec.name, spec.count, round(ms * 1e3, 1), round(spec.flops() / (ms * 1e-3) / 1e12, 1),
+                                 lay.plan.algorithm])
                     del lay
                 configs[net] = {"batch": nb, "convs": sum(sp.count for sp in workload(net, nb)),
                                 "ms_all_convs": round(tot_ms, 4), "tflops": round(tot_flops / (tot_ms * 1e-3) / 1e12, 1),
                                 "images_per_s": round(nb / (tot_ms * 1e-3), 1), "algorithms": algos,
-                                "launches": launches}
+                                "launches": launches, "layers_us_tflops": rows}
                 torch.cuda.empty_cache()
             except Exception as ex:  # report, do not hide
                 configs[net] = {"error": str(ex)}

@@ -13,9 +13,10 @@
 // matrix product.
 //
 // CUDA cores, fp32 FFMA.  One CTA (256 threads) owns an output tile of TP x TQ = 16 x 32
-// pixels of one image for KT = 16 output channels of one group.  Input planes are
+// pixels of one image for KT = 32 output channels of one group.  Input planes are
 // staged PB at a time into shared memory with the padding zeros written in (zero
-// packing).  Each thread accumulates 2 pixels x 16 channels.
+// packing).  Each thread accumulates 2 pixels x 32 channels (64 FFMA per 2 plane samples
+// and 8 broadcast 128-bit scalar loads).
 // Any stride / padding / dilation / groups, NCHW or NHWC in and out, fp32 or bf16.
 #include <cuda_bf16.h>
 #include "internal.h"
@@ -24,7 +25,7 @@
 namespace ai3 {
 
 namespace {
-constexpr int KT = 16, TP = 16, TQ = 32, NT = 256;
+constexpr int KT = 32, TP = 16, TQ = 32, NT = 256;
 
 __device__ __forceinline__ float ld_act(const void* p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
@@ -32,9 +33,9 @@ __device__ __forceinline__ float ld_act(const void* p, int64_t i, int bf16) {
 }  // namespace
 
 // w is the direct layout [G][Cg][R][S][Kgp] (fp32, k fastest): one tap of KT channels is
-// a contiguous 64-byte run, read as four broadcast float4 loads.
+// a contiguous 128-byte run, read as eight broadcast float4 loads.
 template <int KS>
-__global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB, int FH, int FW, int FWp) {
+__global__ void __launch_bounds__(NT, 2) smm_conv_kernel(const DirectArgs a, int PB, int FH, int FW, int FWp) {
     extern __shared__ float smem[];
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(NT) smm_conv_kernel(const DirectArgs a, int PB
 }
 
 // Kgp of the prepared weights must be a multiple of KT (the direct layout pads K per
-// group to 32, which is).
+// group to 64, which is).
 cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st) {
     const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
