@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 //    TMA from L2, at the chip's ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch
 //    runs at 11-12 TB/s of TMA loads),
 // plus a per-tile fill / drain.  Partial last waves count at their own size.
-// mt_ok: two stacked M tiles per unit are allowed (then every B stage feeds 2 x 128 x cg rows,
+// mt_ok: two stacked M tiles per unit are forced (then every B stage feeds 2 x 128 x cg rows,
 // halving B's L2 traffic; at BLOCK_N = 256 the single TMEM buffer costs an epilogue drain
 // per unit that the MMA cannot overlap).
 static int pick_block_n(int Ncols, int M, int batch, int num_groups, int cg, int row_bytes, int num_kb, bool mt_ok,
@@ -1069,7 +1069,7 @@ static int pick_block_n(int Ncols, int M, int batch, int num_groups, int cg, int
     const double kred_bytes = (double)row_bytes * num_kb;  // bytes of one operand row
     int best = 32, best_mt = 1;
     double best_cost = -1;
-    for (int mt = 1; mt <= (mt_ok ? 2 : 1); ++mt) {
+    for (int mt = mt_ok ? 2 : 1; mt <= (mt_ok ? 2 : 1); ++mt) {  // mt_ok: the experiment forces 2
         const long long m_units = (M + 128LL * cg * mt - 1) / (128LL * cg * mt);
         for (int bn : cands) {
             if (bn == 192 && Ncols % 192 != 0) continue;
