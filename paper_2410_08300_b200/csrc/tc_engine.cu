@@ -72,7 +72,7 @@ __host__ __device__ __forceinline__ SmemMap smem_map(const TcArgs& a, int cg, in
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     m.a_bytes = 128u * a.row_bytes;
     m.b_bytes = (uint32_t)(a.block_n / cg) * a.row_bytes;
-    m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (a.mt * m.a_bytes + m.b_bytes);
+    m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (m.a_bytes + m.b_bytes);
     m.bres_off = a.stages * m.stage_bytes;
     m.stg_off = m.bres_off + (uint32_t)a.bres_bytes;
     m.bias_off = m.stg_off + (uint32_t)(num_epi_warps * a.n_stg * 32 * a.stg_row);
@@ -132,7 +132,7 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const int bn_cta = a.block_n / CG;
     const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
-    const uint32_t stage_bytes = splits * (a.mt * a_bytes + b_bytes);
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
     const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
     const int tiles_per_batch = a.m_tiles * a.n_tiles;
     const int total_tiles = tiles_per_batch * a.batch;
@@ -143,56 +143,23 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
         const int b = tile / tiles_per_batch;
         const int rem = tile - b * tiles_per_batch;
         const int mt = rem / a.n_tiles;
-        const int m0 = mt * (BM * CG * a.mt) + (int)rank * BM;
+        const int m0 = mt * (BM * CG) + (int)rank * BM;
         const int n0 = (rem - mt * a.n_tiles) * a.block_n + (int)rank * bn_cta;
-        int n_img = 0, hbase = 0, wbase = 0, n_img1 = 0, hbase1 = 0, wbase1 = 0;
+        int n_img = 0, hbase = 0, wbase = 0;
         if (a.a_mode == TC_A_IM2COL) {
             n_img = m0 / a.PQ;
             const int pq = m0 - n_img * a.PQ;
             const int p = pq / a.Q;
             hbase = p * a.sh - a.ph;
             wbase = (pq - p * a.Q) * a.sw - a.pw;
-            if (a.mt == 2) {  // the second stacked M tile starts BM * CG rows further
-                const int m1 = m0 + BM * CG;
-                n_img1 = m1 / a.PQ;
-                const int pq1 = m1 - n_img1 * a.PQ;
-                const int p1 = pq1 / a.Q;
-                hbase1 = p1 * a.sh - a.ph;
-                wbase1 = (pq1 - p1 * a.Q) * a.sw - a.pw;
-            }
         }
         int cc = 0, ts = 0, tr = 0;  // channel chunk, filter column, filter row of the current K-block
         for (int kb = 0; kb < a.num_kb; ++kb) {
             TRACE_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
             uint8_t* sA = smem + stage * stage_bytes;
-            uint8_t* sB = sA + splits * a.mt * a_bytes;
+            uint8_t* sB = sA + splits * a_bytes;
             const int kx = kb * kelems;
-            if (a.mt == 2) {  // two stacked A tiles + one B slice (bf16, no lo parts)
-                const uint16_t ow = (uint16_t)(ts * a.dw), oh = (uint16_t)(tr * a.dh);
-                if (CG == 1) {
-                    uint64_t* bar = &full[stage];
-                    mbar_arrive_expect_tx(bar, stage_bytes);
-                    if (a.a_mode == TC_A_IM2COL) {
-                        tma_load_im2col_4d(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
-                        tma_load_im2col_4d(sA + a_bytes, &ta0, bar, cc * kelems, wbase1, hbase1, n_img1, ow, oh);
-                    } else {
-                        tma_load_2d(sA, &ta0, bar, kx, m0);
-                        tma_load_2d(sA + a_bytes, &ta0, bar, kx, m0 + BM);
-                    }
-                    tma_load_2d(sB, &tb0, bar, kx, n0);
-                } else {
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
-                    const uint32_t bar = full_base + stage * 8;
-                    if (a.a_mode == TC_A_IM2COL) {
-                        tma_load_im2col_4d_cg2(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
-                        tma_load_im2col_4d_cg2(sA + a_bytes, &ta0, bar, cc * kelems, wbase1, hbase1, n_img1, ow, oh);
-                    } else {
-                        tma_load_2d_cg2(sA, &ta0, bar, kx, m0);
-                        tma_load_2d_cg2(sA + a_bytes, &ta0, bar, kx, m0 + BM * CG);
-                    }
-                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
-                }
-            } else if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
+            if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
                 if (leader) mbar_arrive(&full[stage]);
             } else if (CG == 1) {
                 uint64_t* bar = &full[stage];
@@ -325,12 +292,11 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
     constexpr int splits = CMODE == CM_3XTF32 ? 2 : 1;
     const int bn_cta = a.block_n / CG;
     const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
-    const uint32_t stage_bytes = splits * (a.mt * a_bytes + b_bytes);
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
     const uint32_t idesc = make_idesc(BM * CG, a.block_n, CMODE == CM_BF16 ? 1u : 2u);
     const uint32_t s0 = smem_u32(smem);
     const uint64_t a_desc0 = make_sdesc(s0, a.row_bytes);
-    const uint64_t b_desc0 = make_sdesc(s0 + splits * a.mt * a_bytes, a.row_bytes);
-    const bool two = CMODE == CM_BF16 && a.mt == 2;  // second stacked M tile: +a_bytes in smem, +block_n in TMEM
+    const uint64_t b_desc0 = make_sdesc(s0 + splits * a_bytes, a.row_bytes);
     const uint64_t alo_off = a_bytes >> 4, blo_off = b_bytes >> 4;
     const int tiles = a.m_tiles * a.n_tiles * a.batch;
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
@@ -344,7 +310,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
             if (kc == 0) {
                 TRACE_WAIT(3, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
-                d_tmem = tmem_base + acc * a.block_n * a.mt;
+                d_tmem = tmem_base + acc * a.block_n;
             }
             TRACE_WAIT(2, mbar_wait(&full[stage], phase));
             tc_fence_after();
@@ -358,10 +324,6 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
                     if (CMODE == CM_BF16) {
                         if (CG == 2) mma_bf16_cg2(d_tmem, adk, bdk, idesc, accum);
                         else mma_bf16(d_tmem, adk, bdk, idesc, accum);
-                        if (two) {
-                            if (CG == 2) mma_bf16_cg2(d_tmem + a.block_n, adk + alo_off, bdk, idesc, accum);
-                            else mma_bf16(d_tmem + a.block_n, adk + alo_off, bdk, idesc, accum);
-                        }
                     } else if (CMODE == CM_TF32) {
                         if (CG == 2) mma_tf32_cg2(d_tmem, adk, bdk, idesc, accum);
                         else mma_tf32(d_tmem, adk, bdk, idesc, accum);
@@ -576,13 +538,10 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                         : (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
     int slot = 0, issued = 0;
     const int n_stg = a.n_stg;
-    // mt == 1: the two warpgroups take alternate tiles; mt == 2: both drain every unit, one
-    // stacked M tile each (sub = group)
-    const int sub = a.mt == 2 ? group : 0;
     int it = -1;
     for (int tile = unit; tile < total_tiles; tile += num_units) {
         ++it;
-        if (a.mt != 2 && (it & 1) != group) continue;
+        if ((it & 1) != group) continue;
         const int acc = it % a.n_acc;
         const uint32_t acc_phase = (uint32_t)((it / a.n_acc) & 1);
         int n0, row0, qc = 0, img = 0;
@@ -593,13 +552,13 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
             row0 = hp0 + quarter * (32 / a.TQ);
         } else {
             const int rem = tile % tiles_per_batch;
-            const int m0 = (rem / a.n_tiles) * (BM * CG * a.mt) + sub * (BM * CG) + (int)rank * BM;
+            const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
             n0 = (rem % a.n_tiles) * a.block_n;
             row0 = m0 + quarter * 32;
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const uint32_t tbase = tmem_base + (acc * a.mt + sub) * a.block_n + lane_off;
+        const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
         // 32-column chunks holding real output channels (the last N tile may be partial: its
         // padding columns are never read, and the TMEM release follows the last real chunk)
         const int nvalid = min(ncol32, (a.Ncols - n0 + 31) / 32);
@@ -714,8 +673,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        // mt == 2: both epilogue warpgroups drain every accumulator (one stacked M tile each)
-        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG * a.mt); }
+        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
         mbar_init(bres, 1);
         fence_mbar_init();
     }
@@ -797,7 +755,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.store_mode == 1 && a.stg_row != 0 &&
                           (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
-        if (a.mt == 2 && !fast) __trap();  // stacked M tiles are configured for the fast epilogue only
         if (fast) {
             const uint32_t sb = smem_u32(sbias);
             if (a.a_mode == TC_A_HALO) {
@@ -1060,35 +1017,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 //    TMA from L2, at the chip's ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch
 //    runs at 11-12 TB/s of TMA loads),
 // plus a per-tile fill / drain.  Partial last waves count at their own size.
-// mt_ok: two stacked M tiles per unit are forced (then every B stage feeds 2 x 128 x cg rows,
-// halving B's L2 traffic; at BLOCK_N = 256 the single TMEM buffer costs an epilogue drain
-// per unit that the MMA cannot overlap).
-static int pick_block_n(int Ncols, int M, int batch, int num_groups, int cg, int row_bytes, int num_kb, bool mt_ok,
-                        int* mt_out) {
+static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups, int cg, int row_bytes, int num_kb) {
     const int cands[5] = {32, 64, 128, 192, 256};  // 192: K = 192 / 384 layers (AlexNet) without padding
     const double kred_bytes = (double)row_bytes * num_kb;  // bytes of one operand row
-    int best = 32, best_mt = 1;
+    int best = 32;
     double best_cost = -1;
-    for (int mt = mt_ok ? 2 : 1; mt <= (mt_ok ? 2 : 1); ++mt) {  // mt_ok: the experiment forces 2
-        const long long m_units = (M + 128LL * cg * mt - 1) / (128LL * cg * mt);
-        for (int bn : cands) {
-            if (bn == 192 && Ncols % 192 != 0) continue;
-            if (mt == 2 && (bn < 128 || 512 / (2 * bn) < 1 || bn == 192)) continue;
-            const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
-            const long long full = units / num_groups, rest = units % num_groups;
-            const double mma_cyc = cg == 2 ? (bn >= 128 ? bn / 2.0 : 46.0) : (bn >= 128 ? bn / 2.0 : 66.5);
-            const double t_mma = mt * (double)num_kb * (row_bytes / 32) * mma_cyc;
-            const double tile_bytes = (128.0 * cg * mt + bn) * kred_bytes;
-            const double drain = (mt == 2 && 2 * bn == 512) ? 3000.0 : 0.0;  // single TMEM buffer
-            auto wave = [&](long long u) {
-                const double t_l2 = u * tile_bytes / 6300.0;
-                return (t_mma > t_l2 ? t_mma : t_l2) + 600.0 + drain;
-            };
-            const double cost = full * wave(num_groups) + (rest ? wave(rest) : 0.0);
-            if (best_cost < 0 || cost < best_cost * 0.97) { best = bn; best_mt = mt; best_cost = cost; }
-        }
+    for (int bn : cands) {
+        if (bn == 192 && Ncols % 192 != 0) continue;
+        const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
+        const long long full = units / num_groups, rest = units % num_groups;
+        const double mma_cyc = cg == 2 ? (bn >= 128 ? bn / 2.0 : 46.0) : (bn >= 128 ? bn / 2.0 : 66.5);
+        const double t_mma = (double)num_kb * (row_bytes / 32) * mma_cyc;
+        const double tile_bytes = (128.0 * cg + bn) * kred_bytes;
+        auto wave = [&](long long u) {
+            const double t_l2 = u * tile_bytes / 6300.0;
+            return (t_mma > t_l2 ? t_mma : t_l2) + 600.0;
+        };
+        const double cost = full * wave(num_groups) + (rest ? wave(rest) : 0.0);
+        if (best_cost < 0 || cost < best_cost) { best = bn; best_cost = cost; }
     }
-    *mt_out = best_mt;
     return best;
 }
 
@@ -1110,17 +1057,10 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_BN");  // experiment override: force BLOCK_N
         if (e && atoi(e) > 0) a.block_n = atoi(e);
     }
-    a.mt = 1;
     if (a.block_n == 0) {
         const int cg = pick_cg(a.M);
-        // stacked M tiles (experiment, AI3_MT=2): they need the compile-time bf16 TMA-store
-        // epilogue.  Measured slower on every VGG layer (conv3_2 153 -> 175 us), so off by
-        // default
-        const char* e = getenv("AI3_MT");
-        const bool mt_ok = (e && e[0] == '2') && a.cm == CM_BF16 && a.batch == 1 &&
-                           (a.a_mode == TC_A_IM2COL || a.a_mode == TC_A_TILED2D) && a.out_bf16 && !a.out_nchw &&
-                           a.stg_row != 0 && a.Ncols <= 2048 && cg == 2;
-        a.block_n = pick_block_n(a.Ncols, a.M, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb, mt_ok, &a.mt);
+        const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
+        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb);
     }
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
     if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
@@ -1144,7 +1084,6 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_TC_DEBUG");
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
-    if (a.mt == 2 && (a.store_mode != 1 || !a.epi_fast || a.dbg || a.trace)) a.mt = 1;  // fast epilogue only
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     if (a.a_mode == TC_A_HALO) {
         // one N tile covering every output channel; weights resident per CTA
@@ -1154,8 +1093,7 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.tiles_p = (a.P + a.TP * a.cg - 1) / (a.TP * a.cg);
         a.tiles_q = (a.Q + a.TQ - 1) / a.TQ;
     }
-    const int stage_bytes =
-        a.a_mode == TC_A_HALO ? a.halo_bytes : splits * (a.mt * BM + a.block_n / a.cg) * a.row_bytes;
+    const int stage_bytes = a.a_mode == TC_A_HALO ? a.halo_bytes : splits * (BM + a.block_n / a.cg) * a.row_bytes;
     if (a.bias_smem && a.Ncols > 2048) a.bias_smem = 0;
     const int fixed = 1024 /* barriers */ + 1024 /* alignment slack */ + (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0) +
                       a.bres_bytes;
@@ -1179,13 +1117,13 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.n_tiles = 1;
         a.batch = 1;
     } else {
-        a.m_tiles = (a.M + BM * a.cg * a.mt - 1) / (BM * a.cg * a.mt);  // units of mt stacked M tiles
+        a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
         a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
     }
     p.smem_bytes = stages * stage_bytes + reserve;
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
-    a.n_acc = 512 / (a.block_n * a.mt);
+    a.n_acc = 512 / a.block_n;
     if (a.n_acc > MAX_ACC) a.n_acc = MAX_ACC;
     if (a.cm == CM_3XTF32) {
         // 3xTF32: `nch` accumulation chunks per tile; 2 x nch buffers let the two epilogue
@@ -1193,10 +1131,9 @@ void tc_configure(TcPlan& p, int num_sms) {
         const int nch = (a.num_kb + a.promote_kb - 1) / a.promote_kb;
         a.n_acc = 2 * nch <= a.n_acc ? 2 * nch : 2;
     }
-    if (a.n_acc < 2 && a.mt == 1) a.n_acc = 2;
-    if (a.n_acc < 1) a.n_acc = 1;  // mt == 2 at BLOCK_N = 256: one 512-column buffer
+    if (a.n_acc < 2) a.n_acc = 2;
     int cols = 32;
-    while (cols < a.n_acc * a.block_n * a.mt) cols *= 2;
+    while (cols < a.n_acc * a.block_n) cols *= 2;
     p.tmem_cols = cols;
     const long long units = (long long)a.m_tiles * a.n_tiles * a.batch;  // one unit = one CTA group's tile
     const int max_units = num_sms / a.cg;

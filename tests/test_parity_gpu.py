@@ -225,12 +225,3 @@ def test_execute_host_single_and_pipelined_match_device():
     torch.cuda.synchronize()
     assert torch.equal(y1, want[0])
 
-
-def test_engine_stacked_m_tiles_mode(monkeypatch):
-    """The experimental stacked-M-tile engine mode (AI3_MT=2, off by default)
-    stays correct: bf16 implicit / explicit GEMM layers with several units and ragged tails."""
-    monkeypatch.setenv("AI3_MT", "2")
-    for i, sh in enumerate([ConvShape("mt0", 3, 64, 30, 30, 256, 3, 3, 1, 1), ConvShape("mt1", 2, 128, 28, 28, 128, 3, 3, 1, 1),
-                            ConvShape("mt2", 4, 96, 14, 14, 512, 1, 1)]):
-        for algo in ("implicit_gemm", "gemm"):
-            _check(sh, algo, "bf16", "strict", "nhwc", seed=60 + i)
