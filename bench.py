@@ -173,6 +173,8 @@ class Layer:
             .to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
         wt = torch.from_numpy(w).to(device=device, dtype=torch.bfloat16)
         bt = None if b is None else torch.from_numpy(b).to(device=device, dtype=torch.bfloat16)
+        if algo == "benchmark":  # measure every algorithm once for this layer; the plan takes the winner
+            ai3.autotune(self.x, wt, bt, spec.stride, spec.pad, spec.dil, spec.groups)
         self.plan = ai3.ConvPlan(wt, bt, self.x.shape, spec.stride, spec.pad, spec.dil, spec.groups, algo,
                                  in_layout=1, out_layout=1)
         self.y = torch.empty(self.plan.out_shape, dtype=torch.bfloat16, device=device,
@@ -357,10 +359,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             model_leg = {"error": str(ex)}
 
     # ---- per-algorithm comparison on the same stack (config: Winograd vs implicit GEMM vs direct)
-    per_algo = None
+    per_algo, selector = None, None
     if not args.no_compare and rank == 0:
         per_algo = {}
-        for algo in ("implicit_gemm", "implicit_precomp_gemm", "winograd", "gemm", "kn2row", "direct", "smm"):
+        layer_times = {args.algo: layer_ms}  # per-layer ms of every algorithm on the same stack
+        for algo in ("implicit_gemm", "implicit_precomp_gemm", "winograd", "gemm", "kn2row", "direct", "smm",
+                     "benchmark"):
             if algo == args.algo:
                 per_algo[algo] = round(value / world, 1)
                 continue
@@ -368,12 +372,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 alt = [Layer(s, algo, device, seed=1000 * 2 + i) for i, s in enumerate(specs)]
                 _time_stack(alt, 1, stream, per_layer=False)
                 reps = 3 if algo not in ("direct", "smm") else 1
-                ms, _ = _time_stack(alt, reps, stream, per_layer=False)
+                ms, lms = _time_stack(alt, reps, stream, per_layer=True)
                 per_algo[algo] = round(step_flops / (ms / reps * 1e-3) / 1e12, 1)
+                layer_times[algo] = lms
                 del alt
                 torch.cuda.empty_cache()
             except Exception as ex:  # report, do not hide
                 per_algo[algo] = f"error: {ex}"
+        # selector quality: sum of the chosen algorithms' times over the sum
+        # of the per-layer best among the fixed algorithms (1.0 = never picks a slower one)
+        fixed = [a for a in layer_times if a not in ("guess", "benchmark")]
+        if fixed:
+            best = [min(layer_times[a][i] for a in fixed) for i in range(len(specs))]
+            best_alg = [min(fixed, key=lambda a: layer_times[a][i]) for i in range(len(specs))]
+            selector = {"best_per_layer": dict(zip([l.spec.name for l in layers], best_alg))}
+            for sel in ("guess", "benchmark"):
+                if sel in layer_times:
+                    selector[f"{sel}_regret"] = round(sum(layer_times[sel]) / sum(best), 4)
 
     # ---- oracle on host cores (rank 0, N=1 only)
     cpu = None
@@ -394,7 +409,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                            "l2": "step working set ~2.9 GB of distinct per-layer buffers >> 126 MB L2; no flush"},
                 "images_per_s": images_per_s, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "per_layer": per_layer,
-                "per_algorithm_tflops": per_algo, "vgg16_model": model_leg, "other_configs": configs}
+                "per_algorithm_tflops": per_algo, "selector_quality": selector, "vgg16_model": model_leg,
+                "other_configs": configs}
         print(json.dumps(line), flush=True)
 
 
