@@ -290,6 +290,15 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
                               c.N <= 65535;
         if (allow && shape_ok && pl.Cpad == 64) pl.halo_pb = 128;
         if (allow && shape_ok && c.C <= 8) { pl.halo_pb = 16; pl.Cpad = 8; }
+        // chunked halo: 64-channel chunks of wider inputs, weights streamed per (chunk, tap);
+        // K <= 128 (measured: VGG conv2_2 238 -> 220 us; at K = 256 the im2col mode was as
+        // fast or faster).  AI3_HALO_CHUNKED=0 turns it off (A/B)
+        const char* ec = getenv("AI3_HALO_CHUNKED");
+        const bool allow_c = allow && !(ec && ec[0] == '0');
+        const bool shape_c = algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
+                             c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
+                             c.N <= 65535 && pl.Cpad % 64 == 0 && pl.Cpad >= 128;
+        if (allow_c && shape_c) pl.halo_pb = 128;
     }
     pl.taps_pad = pl.halo_pb == 16 ? round_up(c.R * c.S, 2) : c.R * c.S;
     const size_t wcount = algo == AI3_ALGO_WINOGRAD ? (size_t)16 * c.K * pl.Cpad
@@ -350,6 +359,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         a.sh = 1; a.sw = 1; a.ph = c.ph; a.pw = c.pw; a.dh = 1; a.dw = 1; a.S = (int)c.S; a.R = (int)c.R;
         a.TP = 16; a.TQ = 8; a.RS = 16; a.HR = a.TP + (int)c.R - 1;
         a.halo_pb = pl.halo_pb;
+        a.halo_chunks = pl.halo_pb == 128 ? (int)(pl.Cpad / 64) : 1;
         a.taps_pad = (int)pl.taps_pad;
         a.batch_images = (int)c.N;
         {
@@ -463,7 +473,7 @@ ai3_status encode_b_maps(ai3_plan& pl) {
         const uint64_t kred = (uint64_t)(pl.taps_pad * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
         const uint64_t str[1] = {kred * pl.elem};
-        const uint32_t box[2] = {(uint32_t)pl.Cpad, (uint32_t)(a.block_n / a.cg)};
+        const uint32_t box[2] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)(a.block_n / a.cg)};
         okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box,
                            a.halo_pb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
     } else {
@@ -493,7 +503,7 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
         const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};
         if (a.halo_pb == 128) {
-            const uint32_t box[4] = {(uint32_t)pl.Cpad, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+            const uint32_t box[4] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)a.RS, (uint32_t)a.HR, 1};
             oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
         } else {
             // 16-byte pixels: view the rows as (W*Cpad, H, N) so that each halo row is one

@@ -131,6 +131,10 @@ struct TcArgs {
     int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
     int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B) or 16 (<= 8 channels, no swizzle)
     int taps_pad;   // weight taps held in smem (R*S, rounded up to even for 16-byte pixels)
+    // chunked halo (halo_chunks > 1: Cpad = 64 * halo_chunks channels, K <= 256): per tile and
+    // 64-channel chunk one halo from a ring of hslots; the weights stream per (chunk, tap)
+    // through a ring of bslots instead of staying resident
+    int halo_chunks, hslots, bslots;
     // epilogue
     int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
     int out_bf16;

@@ -74,6 +74,8 @@ __host__ __device__ __forceinline__ SmemMap smem_map(const TcArgs& a, int cg, in
     m.b_bytes = (uint32_t)(a.block_n / cg) * a.row_bytes;
     m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (m.a_bytes + m.b_bytes);
     m.bres_off = a.stages * m.stage_bytes;
+    if (a.a_mode == TC_A_HALO && a.halo_chunks > 1)  // [hslots halos][bslots weight taps]
+        m.bres_off = (uint32_t)(a.hslots * a.halo_bytes + a.bslots * (a.block_n / cg) * 128);
     m.stg_off = m.bres_off + (uint32_t)a.bres_bytes;
     m.bias_off = m.stg_off + (uint32_t)(num_epi_warps * a.n_stg * 32 * a.stg_row);
     m.bar_off = m.bias_off + (a.bias_smem ? ((uint32_t)(a.Ncols * 4 + 15) & ~15u) : 0u);
@@ -511,6 +513,113 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
     }
 }
 
+// ---------------------------------------------------------------- chunked halo (one thread each)
+// C = 64 * halo_chunks channels: for every tile and 64-channel chunk, one halo (HR x RS pixels
+// x 128 B, 128B-swizzled) into the halo ring and R*S weight taps (bn_cta rows x 128 B each)
+// into the tap ring; the MMA reads tap (r, s) of the chunk straight out of the halo.  Each
+// input byte crosses L2 once per (tile, chunk) instead of once per tap (im2col mode).
+// Barriers: full/empty[0 .. hslots) guard the halo ring, [hslots .. hslots+bslots) the taps.
+template <int CG>
+__device__ __forceinline__ void producer_halo_chunked(const TcArgs& a, const CUtensorMap& ta0,
+                                                      const CUtensorMap& tb0, uint8_t* smem, uint64_t* full,
+                                                      uint64_t* empty, uint32_t rank, int unit, int num_units) {
+    const int bn_cta = a.block_n / CG;
+    const uint32_t tap_bytes = (uint32_t)bn_cta * 128u;
+    uint8_t* sH = smem;
+    uint8_t* sT = smem + a.hslots * a.halo_bytes;
+    uint64_t* hfull = full;
+    uint64_t* hempty = empty;
+    uint64_t* tfull_ = full + a.hslots;
+    uint64_t* tempty_ = empty + a.hslots;
+    const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+    const int taps = a.R * a.S;
+    const int n0 = (int)rank * bn_cta;
+    int hs = 0, ts = 0;
+    uint32_t hph = 0, tph = 0;
+    for (int tile = unit; tile < a.m_tiles; tile += num_units) {
+        int n, p0, q0;
+        halo_tile(a, tile, CG, rank, n, p0, q0);
+        for (int c = 0; c < a.halo_chunks; ++c) {
+            mbar_wait(&hempty[hs], hph ^ 1);
+            if (CG == 1) {
+                mbar_arrive_expect_tx(&hfull[hs], (uint32_t)a.halo_bytes);
+                tma_load_4d(sH + hs * a.halo_bytes, &ta0, &hfull[hs], c * 64, q0 - a.pw, p0 - a.ph, n);
+            } else {
+                if (rank == 0) mbar_arrive_expect_tx(&hfull[hs], 2u * (uint32_t)a.halo_bytes);
+                tma_load_4d_cg2(sH + hs * a.halo_bytes, &ta0, full_base + hs * 8, c * 64, q0 - a.pw, p0 - a.ph, n);
+            }
+            if (++hs == a.hslots) { hs = 0; hph ^= 1; }
+            for (int t = 0; t < taps; ++t) {
+                mbar_wait(&tempty_[ts], tph ^ 1);
+                const int kx = t * a.halo_chunks * 64 + c * 64;  // column of (tap, chunk) in [K][R*S][Cpad]
+                if (CG == 1) {
+                    mbar_arrive_expect_tx(&tfull_[ts], tap_bytes);
+                    tma_load_2d(sT + ts * tap_bytes, &tb0, &tfull_[ts], kx, n0);
+                } else {
+                    if (rank == 0) mbar_arrive_expect_tx(&tfull_[ts], 2u * tap_bytes);
+                    tma_load_2d_cg2(sT + ts * tap_bytes, &tb0, full_base + (a.hslots + ts) * 8, kx, n0);
+                }
+                if (++ts == a.bslots) { ts = 0; tph ^= 1; }
+            }
+        }
+    }
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_issuer_halo_chunked(const TcArgs& a, uint8_t* smem, uint64_t* full,
+                                                        uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
+                                                        uint32_t tmem_base, int unit, int num_units) {
+    const int bn_cta = a.block_n / CG;
+    const uint32_t tap_bytes = (uint32_t)bn_cta * 128u;
+    const uint32_t idesc = make_idesc(BM * CG, a.block_n, 1u);
+    const uint32_t s0 = smem_u32(smem);
+    const uint32_t sT = s0 + a.hslots * a.halo_bytes;
+    const uint64_t a0 = make_sdesc_sw128(s0, (uint32_t)a.RS * 128u, 0u);
+    const uint64_t b0 = make_sdesc_sw128(sT, 1024u, 0u);
+    uint64_t* hfull = full;
+    uint64_t* hempty = empty;
+    uint64_t* wfull = full + a.hslots;
+    uint64_t* wempty = empty + a.hslots;
+    const int taps = a.R * a.S;
+    int hs = 0, ts = 0, acc = 0;
+    uint32_t hph = 0, tph = 0, acc_phase = 0;
+    for (int tile = unit; tile < a.m_tiles; tile += num_units) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * a.block_n;
+        for (int c = 0; c < a.halo_chunks; ++c) {
+            mbar_wait(&hfull[hs], hph);
+            tc_fence_after();
+            const uint64_t ah = a0 + (uint64_t)((hs * a.halo_bytes) >> 4);
+            int t = 0;
+            for (int r = 0; r < a.R; ++r) {
+                for (int sx = 0; sx < a.S; ++sx, ++t) {
+                    mbar_wait(&wfull[ts], tph);
+                    tc_fence_after();
+                    const uint64_t ad = ah + (uint64_t)((r * a.RS + sx) * 8);  // tap view: (r*RS + s) rows in
+                    const uint64_t bd = b0 + (uint64_t)((ts * tap_bytes) >> 4);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t accum = (c > 0 || t > 0 || k > 0) ? 1u : 0u;
+                        if (CG == 2) mma_bf16_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                        else mma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
+                    }
+                    if (CG == 2) mma_commit_cg2(&wempty[ts], 0x3);
+                    else mma_commit(&wempty[ts]);
+                    if (++ts == a.bslots) { ts = 0; tph ^= 1; }
+                }
+            }
+            (void)taps;
+            if (CG == 2) mma_commit_cg2(&hempty[hs], 0x3);
+            else mma_commit(&hempty[hs]);
+            if (++hs == a.hslots) { hs = 0; hph ^= 1; }
+        }
+        if (CG == 2) mma_commit_cg2(&tfull[acc], 0x3);
+        else mma_commit(&tfull[acc]);
+        if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
+    }
+}
+
 // ---------------------------------------------------------------- fast epilogue
 // The common case -- bf16 NHWC output through TMA stores, bias (if any) staged in smem,
 // one accumulation chunk per tile -- with every configuration choice resolved at compile
@@ -698,7 +807,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (warp == 0) {
         if (elect_one()) {
             TRACE_WAIT(1, {
-                if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);
+                if (a.a_mode == TC_A_HALO && a.halo_chunks > 1)
+                    producer_halo_chunked<CG>(a, ta0, tb0, smem, full, empty, rank, unit, num_units);
+                else if (a.a_mode == TC_A_HALO) producer_halo<CG>(a, ta0, tb0, smem, full, empty, bres, rank, unit, num_units);
                 else producer<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units);
             });
         }
@@ -708,7 +819,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // kind and on the number of 32-byte K slices per K-block (1, 2 or 4).
         const bool elected = elect_one();  // one elect.sync for the whole warp
         const unsigned long long t_mma0 = clock64();
-        if (leader && elected && a.a_mode == TC_A_HALO) {
+        if (leader && elected && a.a_mode == TC_A_HALO && a.halo_chunks > 1) {
+            mma_issuer_halo_chunked<CG>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
+        } else if (leader && elected && a.a_mode == TC_A_HALO) {
             if (a.R == 3 && a.S == 3 && a.RS == 16)
                 mma_issuer_halo<CG, 1>(a, smem, full, empty, tfull, tempty, bres, tmem_base, unit, num_units);
             else
@@ -1085,11 +1198,12 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
+    const bool chunked = a.a_mode == TC_A_HALO && a.halo_chunks > 1;
     if (a.a_mode == TC_A_HALO) {
-        // one N tile covering every output channel; weights resident per CTA
-        a.block_n = a.Ncols <= 32 ? 32 : (a.Ncols <= 64 ? 64 : 128);
+        // one N tile covering every output channel; weights resident per CTA (chunked: streamed)
+        a.block_n = a.Ncols <= 32 ? 32 : (a.Ncols <= 64 ? 64 : (a.Ncols <= 128 ? 128 : 256));
         a.halo_bytes = a.HR * a.RS * a.halo_pb;
-        a.bres_bytes = a.taps_pad * (a.block_n / a.cg) * a.halo_pb;
+        a.bres_bytes = chunked ? 0 : a.taps_pad * (a.block_n / a.cg) * a.halo_pb;
         a.tiles_p = (a.P + a.TP * a.cg - 1) / (a.TP * a.cg);
         a.tiles_q = (a.Q + a.TQ - 1) / a.TQ;
     }
@@ -1108,10 +1222,20 @@ void tc_configure(TcPlan& p, int num_sms) {
         if (stages_for(4) >= base_stages) a.n_stg = 4;          // room to spare: deeper store queue
         else if (base_stages < 6 && stages_for(1) > base_stages) a.n_stg = 1;  // long-K tiles: operand ring first
     }
-    const int reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
+    int reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
     int stages = stages_for(a.n_stg);
     if (stages < 2) stages = 2;
     a.stages = stages;
+    if (chunked) {
+        // two halos + as many weight-tap slots as fit (>= 4), one store buffer per epilogue warp
+        a.n_stg = 1;
+        reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
+        const int tap_bytes = (a.block_n / a.cg) * 128;
+        a.hslots = 2;
+        int bs = (SMEM_LIMIT - reserve - a.hslots * a.halo_bytes) / tap_bytes;
+        a.bslots = bs > 8 ? 8 : bs;
+        a.stages = a.hslots + a.bslots;  // barrier pairs: halo ring, then tap ring
+    }
     if (a.a_mode == TC_A_HALO) {
         a.m_tiles = a.batch_images * a.tiles_p * a.tiles_q;  // units: one (image, p-band, q-band) per CTA group
         a.n_tiles = 1;
@@ -1120,7 +1244,8 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
         a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
     }
-    p.smem_bytes = stages * stage_bytes + reserve;
+    p.smem_bytes = chunked ? a.hslots * a.halo_bytes + a.bslots * (a.block_n / a.cg) * 128 + reserve
+                           : stages * stage_bytes + reserve;
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
     a.n_acc = 512 / a.block_n;

@@ -66,6 +66,8 @@ RAGGED = [
     ConvShape("r3x3d2", 2, 32, 19, 19, 32, 3, 3, 1, 2, 2),
     ConvShape("r3x3s2", 2, 128, 28, 28, 128, 3, 3, 2, 1),
     ConvShape("rodd", 1, 16, 9, 7, 24, 3, 3, 1, 0),       # odd P, Q: Winograd crop
+    ConvShape("rhalo2", 2, 128, 21, 27, 96, 3, 3, 1, 1),  # chunked halo: 2 channel chunks, ragged tiles
+    ConvShape("rhalo3", 1, 192, 17, 13, 64, 5, 5, 1, 2),  # chunked halo: 3 chunks, 5x5 taps
 ]
 
 
