@@ -362,12 +362,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     per_algo, selector = None, None
     if not args.no_compare and rank == 0:
         per_algo = {}
-        layer_times = {args.algo: layer_ms}  # per-layer ms of every algorithm on the same stack
+        layer_times = {}  # per-layer ms of every algorithm on the same stack, timed the same way
         for algo in ("implicit_gemm", "implicit_precomp_gemm", "winograd", "gemm", "kn2row", "direct", "smm",
-                     "benchmark"):
-            if algo == args.algo:
-                per_algo[algo] = round(value / world, 1)
-                continue
+                     "guess", "benchmark"):
             try:
                 alt = [Layer(s, algo, device, seed=1000 * 2 + i) for i, s in enumerate(specs)]
                 _time_stack(alt, 1, stream, per_layer=False)
