@@ -198,6 +198,83 @@ __global__ void __launch_bounds__(256) im2col_smallc_kernel(const void* __restri
     }
 }
 
+// Vectorised NHWC variant (C a multiple of V, bf16 -> bf16 or fp32 -> any mode): one warp
+// per output pixel row of A.  The pixel (n, p, q) is decoded once per row; lane l writes
+// 16-byte groups g = l, l + 32, ... whose (tap, channel) coordinates advance by carries
+// (32 * V channels per step), so the inner loop has no division.  Loads and stores are
+// both 16-byte and coalesced across the warp.
+template <bool BF16IN, int V>
+__global__ void __launch_bounds__(256) im2col_rows_kernel(const void* __restrict__ xin, int64_t N, int C, int H, int W,
+                                                          int P, int Q, int R, int S, int sh, int sw, int ph, int pw,
+                                                          int dh, int dw, int Kp, int cm, void* A, void* A_lo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t M = N * P * Q;
+    const int groups = Kp / V;
+    const int kred_groups = R * S * C / V;  // groups inside the exact reduction length
+    const int step_c = 32 * V;              // channels a lane advances per iteration
+    const int dtap = step_c / C, dc = step_c - (step_c / C) * C;
+    for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < M;
+         m += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t n = m / ((int64_t)P * Q);
+        const int pq = (int)(m - n * P * Q);
+        const int p = pq / Q, q = pq - (pq / Q) * Q;
+        const int ih0 = p * sh - ph, iw0 = q * sw - pw;
+        const int64_t xrow = n * H;
+        // coordinates of this lane's first group
+        int c = lane * V, tap = 0;
+        while (c >= C) { c -= C; ++tap; }
+        int r = tap / S, sx = tap - (tap / S) * S;
+        for (int g = lane; g < groups; g += 32) {
+            float vals[V];
+            if (g < kred_groups) {
+                const int ih = ih0 + r * dh, iw = iw0 + sx * dw;
+                if (ih >= 0 && ih < H && iw >= 0 && iw < W) {
+                    const int64_t off = ((xrow + ih) * W + iw) * C + c;
+                    if (BF16IN) {
+                        const uint4 raw = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(xin) + off);
+                        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+                        for (int v = 0; v < V; ++v) vals[v] = __bfloat162float(e[v]);
+                    } else {
+                        const float4 raw = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xin) + off);
+                        vals[0] = raw.x; vals[1] = raw.y; vals[2] = raw.z; vals[3] = raw.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) vals[v] = 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) vals[v] = 0.f;
+            }
+            const int64_t o = m * groups + g;
+            if (cm == CM_BF16) {
+                __align__(16) __nv_bfloat16 h[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) h[v] = __float2bfloat16_rn(vals[v]);
+                reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(h);
+            } else if (cm == CM_TF32) {
+                __align__(16) float h[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) h[v] = tf32_round(vals[v]);
+                reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(h);
+            } else {
+                __align__(16) float hi[V], lo[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) { hi[v] = tf32_round(vals[v]); lo[v] = tf32_round(vals[v] - hi[v]); }
+                reinterpret_cast<uint4*>(A)[o] = *reinterpret_cast<const uint4*>(hi);
+                reinterpret_cast<uint4*>(A_lo)[o] = *reinterpret_cast<const uint4*>(lo);
+            }
+            // advance by 32 groups = step_c channels: carry into the tap, then into (r, s)
+            c += dc;
+            int t = dtap + (c >= C ? 1 : 0);
+            if (c >= C) c -= C;
+            sx += t;
+            while (sx >= S) { sx -= S; ++r; }
+        }
+    }
+}
+
 cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
                           int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t Kp,
                           ComputeMode cm, void* A, void* A_lo, cudaStream_t st) {
@@ -225,10 +302,24 @@ cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t
         }
     }
     const int V = cm == CM_BF16 ? 8 : 4;
+    const int nhwc = in_layout == AI3_NHWC;
+    // the input element width must equal the operand element width for a 16-byte group to be
+    // one 16-byte load: bf16 -> bf16 (V = 8) or fp32 -> tf32 / 3xTF32 (V = 4)
+    if (nhwc && C % V == 0 && ((dtype == AI3_BF16) == (cm == CM_BF16)) && (R * S * C) % V == 0) {
+        const int64_t warps = N * P * Q;
+        const int64_t blocks = (warps * 32 + 255) / 256;
+        const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
+        if (dtype == AI3_BF16)
+            im2col_rows_kernel<true, 8><<<grid, 256, 0, st>>>(x, N, (int)C, (int)H, (int)W, (int)P, (int)Q, R, S, sh,
+                                                               sw, ph, pw, dh, dw, (int)Kp, cm, A, A_lo);
+        else
+            im2col_rows_kernel<false, 4><<<grid, 256, 0, st>>>(x, N, (int)C, (int)H, (int)W, (int)P, (int)Q, R, S, sh,
+                                                                sw, ph, pw, dh, dw, (int)Kp, cm, A, A_lo);
+        return cudaGetLastError();
+    }
     const int64_t total = N * P * Q * (Kp / V);
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 64 ? blocks : 148 * 64);
-    const int nhwc = in_layout == AI3_NHWC;
     if (dtype == AI3_BF16) {
         if (V == 8) im2col_kernel<true, 8><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
         else im2col_kernel<true, 4><<<grid, 256, 0, st>>>(x, nhwc, N, C, H, W, P, Q, R, S, sh, sw, ph, pw, dh, dw, Kp, cm, A, A_lo);
