@@ -114,7 +114,9 @@ ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
     switch (algo) {
         case AI3_ALGO_GUESS:
         case AI3_ALGO_BENCHMARK:
+            return ok();
         case AI3_ALGO_DIRECT:
+            if (c.N * c.G > 65535) return fail(AI3_ERR_UNSUPPORTED, "direct: N*groups > 65535 (one grid row per image/group)");
             return ok();
         case AI3_ALGO_IMPLICIT_GEMM: {
             if (c.G != 1)
@@ -203,6 +205,7 @@ ai3_status resolve_algo(const ConvProblem& c, ai3_algo algo, ai3_algo* out) {
         return ok();
     }
     *out = algo == AI3_ALGO_GUESS ? guess_rule(c) : algo;
+    if (algo == AI3_ALGO_GUESS) return check_supported(c, *out);  // e.g. grouped convs beyond direct's grid
     return ok();
 }
 
