@@ -132,9 +132,9 @@ def test_workspace_sizes():
     # Winograd: 16 transformed tiles in (V) and out (M, fp32)
     T = 64 * 28 * 28
     assert ws((64, 256, 56, 56), 256, 3, "winograd") >= 16 * T * 256 * 2 + 16 * T * 256 * 4
-    # direct needs no workspace beyond the fp32 weights
-    # direct: fp32 weights [Cg][R][S][K padded to 32] + fp32 bias, each region 256-byte aligned
-    assert ws((2, 3, 32, 32), 16, 3, "direct", dtype=_lib.F32) == 3584 + 256
+    # direct needs no workspace beyond the fp32 weights [Cg][R][S][K padded to 64] and the fp32
+    # bias, each region 256-byte aligned: 3*3*3*64*4 = 6912 (already aligned) + 256
+    assert ws((2, 3, 32, 32), 16, 3, "direct", dtype=_lib.F32) == 6912 + 256
 
 
 def test_null_and_bad_arguments():
