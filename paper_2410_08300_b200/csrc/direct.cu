@@ -69,22 +69,23 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     for (int c0 = 0; c0 < a.Cg; c0 += CB) {
         const int cb = min(CB, a.Cg - c0);
         // ---- stage the input footprint (zeros outside the image)
+        // ---- weights [cc][r][s][TK]: contiguous 16-byte pieces of the prepared rows, copied
+        //      asynchronously (cp.async) so they stream in while the footprint is staged
+        {
+            const int nq = cb * R * S * (TK / 4);
+            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+            for (int i = tid; i < nq; i += NT) {
+                const int row = i / (TK / 4), qd = i % (TK / 4);  // row (cc, r, s), 4-channel piece
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + row * TK + 4 * qd);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
                             ih0, iw0, cb, FH, FW, FWp, tid);
-        // ---- stage weights [cc][r][s][TK] (contiguous rows of the prepared layout)
-        const int nw = cb * R * S * TK;
-        const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
-        for (int base = 0; base < nw; base += NT * 4) {  // 4 loads in flight per thread
-            float v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int idx = base + u * NT + tid;
-                v[u] = idx < nw ? wsrc[(int64_t)(idx / TK) * a.Kgp + idx % TK] : 0.f;  // row (cc, r, s), column k
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (base + u * NT + tid < nw) ws[base + u * NT + tid] = v[u];
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         for (int cc = 0; cc < cb; ++cc) {
 #pragma unroll
