@@ -65,22 +65,23 @@ __global__ void __launch_bounds__(NT, 2) smm_conv_kernel(const DirectArgs a, int
     for (int c0 = 0; c0 < a.Cg; c0 += PB) {
         const int pb = min(PB, a.Cg - c0);
         // ---- zero-packed planes of channels c0 .. c0+pb-1 (padding written as zeros)
+        // ---- the scalars w[k0g .. k0g+KT)[c][r][s]: 16-byte pieces copied asynchronously while
+        //      the planes are staged
+        {
+            const int nq = pb * R * S * (KT / 4);
+            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+            for (int i = tid; i < nq; i += NT) {
+                const int row = i / (KT / 4), qd = i % (KT / 4);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wsm + row * KT + 4 * qd);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
                             ih0, iw0, pb, FH, FW, FWp, tid);
-        // ---- the scalars: w[k0g .. k0g+KT)[c][r][s]
-        const int nw = pb * R * S * KT;
-        const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
-        for (int base = 0; base < nw; base += NT * 4) {  // 4 loads in flight per thread
-            float v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int idx = base + u * NT + tid;
-                v[u] = idx < nw ? wsrc[(int64_t)(idx / KT) * a.Kgp + idx % KT] : 0.f;  // row (cc, r, s), column k
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (base + u * NT + tid < nw) wsm[base + u * NT + tid] = v[u];
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         for (int cc = 0; cc < pb; ++cc) {
             const float* X = xs + cc * plane;
