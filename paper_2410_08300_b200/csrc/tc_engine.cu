@@ -1227,13 +1227,19 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (stages < 2) stages = 2;
     a.stages = stages;
     if (chunked) {
-        // two halos + as many weight-tap slots as fit (>= 4), one store buffer per epilogue warp
-        a.n_stg = 1;
+        // two halos + as many weight-tap slots as fit, n_stg store buffers per epilogue warp
+        {
+            const char* es = getenv("AI3_HALO_NSTG");
+            a.n_stg = (es && (es[0] == '1' || es[0] == '2' || es[0] == '4')) ? es[0] - '0' : 1;
+        }
         reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
         const int tap_bytes = (a.block_n / a.cg) * 128;
-        a.hslots = 2;
+        const char* eh = getenv("AI3_HSLOTS");
+        const char* eb = getenv("AI3_BSLOTS");
+        a.hslots = (eh && atoi(eh) >= 2) ? atoi(eh) : 2;
         int bs = (SMEM_LIMIT - reserve - a.hslots * a.halo_bytes) / tap_bytes;
-        a.bslots = bs > 8 ? 8 : bs;
+        const int bcap = (eb && atoi(eb) >= 2) ? atoi(eb) : 16;  // a deep tap ring hides the weight loads' latency
+        a.bslots = bs > bcap ? bcap : bs;
         a.stages = a.hslots + a.bslots;  // barrier pairs: halo ring, then tap ring
     }
     if (a.a_mode == TC_A_HALO) {
