@@ -63,18 +63,22 @@ cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K
 
 // One thread per (output pixel, VK consecutive output channels): VK-wide loads of the
 // R*S partial rows (consecutive threads read consecutive channels of one row).
-template <int VK>
+// IDX: uint32_t when the thread count fits (64-bit divisions would dominate this HBM-bound pass).
+template <int VK, typename IDX>
 __global__ void kn2row_accumulate_kernel(const float* __restrict__ Z, const float* __restrict__ bias, void* y,
                                          int out_nhwc, int bf16, int64_t N, int64_t H, int64_t W, int64_t K,
                                          int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh,
                                          int dw, int relu) {
-    const int64_t kg = K / VK;
-    const int64_t total = N * P * Q * kg;
+    const IDX kg = (IDX)(K / VK);
+    const IDX total = (IDX)(N * P * Q * (int64_t)kg);
     const int64_t zrow = (int64_t)R * S * K;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k0 = (i % kg) * VK;
-        const int64_t m = i / kg;
-        const int64_t q = m % Q, p = (m / Q) % P, n = m / (P * Q);
+    const IDX Qi = (IDX)Q, Pi = (IDX)P;
+    for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
+        const IDX mi = i / kg;
+        const int64_t k0 = (int64_t)(i - mi * kg) * VK;
+        const int64_t m = mi;
+        const IDX mq = mi / Qi;
+        const int64_t q = mi - mq * Qi, p = mq % Pi, n = mq / Pi;
         float acc[VK];
 #pragma unroll
         for (int v = 0; v < VK; ++v) acc[v] = 0.f;
@@ -112,12 +116,19 @@ cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y,
     const int VK = K % 4 == 0 ? 4 : 1;
     const int64_t total = N * P * Q * (K / VK);
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    if (VK == 4)
-        kn2row_accumulate_kernel<4><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S, sh, sw,
-                                                          ph, pw, dh, dw, relu);
+    const bool small = total < (1LL << 31);
+    if (VK == 4 && small)
+        kn2row_accumulate_kernel<4, uint32_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
+                                                                    sh, sw, ph, pw, dh, dw, relu);
+    else if (VK == 4)
+        kn2row_accumulate_kernel<4, int64_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
+                                                                   sh, sw, ph, pw, dh, dw, relu);
+    else if (small)
+        kn2row_accumulate_kernel<1, uint32_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
+                                                                    sh, sw, ph, pw, dh, dw, relu);
     else
-        kn2row_accumulate_kernel<1><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S, sh, sw,
-                                                          ph, pw, dh, dw, relu);
+        kn2row_accumulate_kernel<1, int64_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
+                                                                   sh, sw, ph, pw, dh, dw, relu);
     return cudaGetLastError();
 }
 

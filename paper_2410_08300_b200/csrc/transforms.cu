@@ -339,19 +339,24 @@ __device__ __forceinline__ float bt_comb(const float (&r)[4], int a) {
     return a == 0 ? r[0] - r[2] : (a == 1 ? r[1] + r[2] : (a == 2 ? r[2] - r[1] : r[1] - r[3]));
 }
 
-template <bool BF16IN>
+// IDX: the index type of the decomposition (uint32_t when T * Cpad / 4 < 2^31: the 64-bit
+// divisions otherwise dominate the instruction count of this memory-bound kernel).
+template <bool BF16IN, typename IDX>
 __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restrict__ xin, int64_t N, int64_t H,
                                                              int64_t W, int64_t Cpad, int64_t TH, int64_t TW, int ph,
                                                              int pw, int cm, void* V, void* V_lo) {
     constexpr int VC = 4;
-    const int64_t groups = Cpad / VC;
+    const IDX groups = (IDX)(Cpad / VC);
     const int64_t T = N * TH * TW;
-    const int64_t total = T * groups;
+    const IDX total = (IDX)(T * (int64_t)groups);
     const int64_t plane = T * Cpad;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / groups, cgi = i % groups;
-        const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
-        const int64_t ih0 = 2 * th - ph, iw0 = 2 * tw - pw;
+    const IDX tht = (IDX)(TH * TW), tw_ = (IDX)TW, th_ = (IDX)TH;
+    for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
+        const IDX t = i / groups, cgi = i - (i / groups) * groups;
+        const IDX n = t / tht, rem = t - n * tht;
+        const IDX th = rem / tw_, tw = rem - (rem / tw_) * tw_;
+        (void)th_;
+        const int64_t ih0 = 2 * (int64_t)th - ph, iw0 = 2 * (int64_t)tw - pw;
         float d[4][4][VC];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restr
             for (int b = 0; b < 4; ++b) {
                 const int64_t ih = ih0 + a, iw = iw0 + b;
                 const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
-                const int64_t off = ((n * H + ih) * W + iw) * Cpad + cgi * VC;
+                const int64_t off = (((int64_t)n * H + ih) * W + iw) * Cpad + (int64_t)cgi * VC;
                 if (BF16IN) {
                     const uint2 raw = ok ? *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(xin) + off)
                                          : make_uint2(0, 0);
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restr
                 }
             }
         }
-        const int64_t base = t * Cpad + cgi * VC;
+        const int64_t base = (int64_t)t * Cpad + (int64_t)cgi * VC;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             float bt[4][VC];  // row a of B^T d, per channel
@@ -418,10 +423,14 @@ cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W
     const int64_t total = N * TH * TW * (Cpad / 4);
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-    if (cm == CM_BF16)
-        winograd_input_kernel<true><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
-    else
-        winograd_input_kernel<false><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+    const bool small = total < (1LL << 31);
+    if (cm == CM_BF16) {
+        if (small) winograd_input_kernel<true, uint32_t><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+        else winograd_input_kernel<true, int64_t><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+    } else {
+        if (small) winograd_input_kernel<false, uint32_t><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+        else winograd_input_kernel<false, int64_t><<<grid, 256, 0, st>>>(x, N, H, W, Cpad, TH, TW, ph, pw, cm, V, V_lo);
+    }
     return cudaGetLastError();
 }
 
