@@ -97,15 +97,20 @@ struct PoolGeom {
 };
 
 // NHWC, one thread per (pixel, 16-byte channel group)
-template <bool BF16, bool MAX>
+// IDX: uint32_t when the thread count fits (the 64-bit index divisions would otherwise
+// dominate this HBM-bound kernel's instruction count).
+template <bool BF16, bool MAX, typename IDX>
 __global__ void pool_nhwc_kernel(const void* __restrict__ x, void* y, PoolGeom g) {
     constexpr int V = Vec<BF16>::N;
-    const int64_t cg = g.C / V;
-    const int64_t total = g.N * g.P * g.Q * cg;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c0 = (i % cg) * V;
-        const int64_t m = i / cg;
-        const int64_t q = m % g.Q, p = (m / g.Q) % g.P, n = m / (g.P * g.Q);
+    const IDX cg = (IDX)(g.C / V);
+    const IDX total = (IDX)(g.N * g.P * g.Q * (int64_t)cg);
+    const IDX Qi = (IDX)g.Q, Pi = (IDX)g.P;
+    for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
+        const IDX mi = i / cg;
+        const int64_t c0 = (int64_t)(i - mi * cg) * V;
+        const int64_t m = mi;
+        const IDX mq = mi / Qi;
+        const int64_t q = mi - mq * Qi, p = mq % Pi, n = mq / Pi;
         float acc[V];
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[j] = MAX ? -INFINITY : 0.f;
@@ -311,12 +316,14 @@ static ai3_status pool_common(const ai3_tensor4d* x, const ai3_pool2d_params* p,
     if (vec) {
         const int64_t work = g.N * g.P * g.Q * (g.C / V);
         const int grid = grid_for(work, 256);
+        const bool small = work < (1LL << 31);
+        auto go = [&](auto kern) { kern<<<grid, 256, 0, st>>>(x->data, y->data, g); };
         if (bf16) {
-            if (is_max) pool_nhwc_kernel<true, true><<<grid, 256, 0, st>>>(x->data, y->data, g);
-            else pool_nhwc_kernel<true, false><<<grid, 256, 0, st>>>(x->data, y->data, g);
+            if (is_max) small ? go(pool_nhwc_kernel<true, true, uint32_t>) : go(pool_nhwc_kernel<true, true, int64_t>);
+            else small ? go(pool_nhwc_kernel<true, false, uint32_t>) : go(pool_nhwc_kernel<true, false, int64_t>);
         } else {
-            if (is_max) pool_nhwc_kernel<false, true><<<grid, 256, 0, st>>>(x->data, y->data, g);
-            else pool_nhwc_kernel<false, false><<<grid, 256, 0, st>>>(x->data, y->data, g);
+            if (is_max) small ? go(pool_nhwc_kernel<false, true, uint32_t>) : go(pool_nhwc_kernel<false, true, int64_t>);
+            else small ? go(pool_nhwc_kernel<false, false, uint32_t>) : go(pool_nhwc_kernel<false, false, int64_t>);
         }
     } else {
         pool_scalar_kernel<<<grid_for(g.N * g.C * g.P * g.Q, 256), 256, 0, st>>>(x->data, y->data, g, nhwc, bf16,

@@ -491,16 +491,18 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
 }
 
 // NHWC output, K % 4 == 0: one thread per (tile, 4 output channels).
+template <typename IDX>
 __global__ void __launch_bounds__(256) winograd_output_nhwc4_kernel(const float* __restrict__ M,
                                                                     const float* __restrict__ bias, void* y, int bf16,
                                                                     int64_t N, int64_t K, int64_t P, int64_t Q,
                                                                     int64_t TH, int64_t TW, int relu) {
     const int64_t T = N * TH * TW;
-    const int64_t kg = K / 4;
-    const int64_t total = T * kg;
+    const IDX kg = (IDX)(K / 4);
+    const IDX total = (IDX)(T * (int64_t)kg);
     const int64_t plane = T * K;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / kg, k0 = (i % kg) * 4;
+    for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
+        const IDX ti = i / kg;
+        const int64_t t = ti, k0 = (int64_t)(i - ti * kg) * 4;
         const int64_t off = t * K + k0;
         float4 mv[16];
 #pragma unroll
@@ -513,7 +515,9 @@ __global__ void __launch_bounds__(256) winograd_output_nhwc4_kernel(const float*
             for (int j = 0; j < 16; ++j) m[j / 4][j % 4] = v == 0 ? mv[j].x : (v == 1 ? mv[j].y : (v == 2 ? mv[j].z : mv[j].w));
             wino_out4(m, bias ? bias[k0 + v] : 0.f, relu, out[v]);
         }
-        const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
+        const IDX thw = (IDX)(TH * TW), twi = (IDX)TW;
+        const IDX ni = ti / thw, rem = ti - ni * thw;
+        const int64_t n = ni, th = rem / twi, tw = rem - (rem / twi) * twi;
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
             const int64_t p = 2 * th + a;
@@ -543,7 +547,10 @@ cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, 
         const int64_t total = N * TH * TW * (K / 4);
         const int64_t blocks = (total + 255) / 256;
         const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-        winograd_output_nhwc4_kernel<<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
+        if (total < (1LL << 31))
+            winograd_output_nhwc4_kernel<uint32_t><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
+        else
+            winograd_output_nhwc4_kernel<int64_t><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
         return cudaGetLastError();
     }
     const int64_t total = N * TH * TW * K;
