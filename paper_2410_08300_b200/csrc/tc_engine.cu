@@ -72,7 +72,7 @@ __host__ __device__ __forceinline__ SmemMap smem_map(const TcArgs& a, int cg, in
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     m.a_bytes = 128u * a.row_bytes;
     m.b_bytes = (uint32_t)(a.block_n / cg) * a.row_bytes;
-    m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (m.a_bytes + m.b_bytes);
+    m.stage_bytes = a.a_mode == TC_A_HALO ? (uint32_t)a.halo_bytes : splits * (m.a_bytes + a.n2 * m.b_bytes);
     m.bres_off = a.stages * m.stage_bytes;
     if (a.a_mode == TC_A_HALO && a.halo_chunks > 1)  // [hslots halos][bslots weight taps]
         m.bres_off = (uint32_t)(a.hslots * a.halo_bytes + a.bslots * (a.block_n / cg) * 128);
@@ -134,7 +134,7 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const int bn_cta = a.block_n / CG;
     const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
-    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const uint32_t stage_bytes = splits * (a_bytes + a.n2 * b_bytes);
     const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
     const int tiles_per_batch = a.m_tiles * a.n_tiles;
     const int total_tiles = tiles_per_batch * a.batch;
@@ -146,7 +146,7 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
         const int rem = tile - b * tiles_per_batch;
         const int mt = rem / a.n_tiles;
         const int m0 = mt * (BM * CG) + (int)rank * BM;
-        const int n0 = (rem - mt * a.n_tiles) * a.block_n + (int)rank * bn_cta;
+        const int n0 = (rem - mt * a.n_tiles) * a.block_n * a.n2 + (int)rank * bn_cta;
         int n_img = 0, hbase = 0, wbase = 0;
         if (a.a_mode == TC_A_IM2COL) {
             n_img = m0 / a.PQ;
@@ -161,7 +161,25 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
             uint8_t* sA = smem + stage * stage_bytes;
             uint8_t* sB = sA + splits * a_bytes;
             const int kx = kb * kelems;
-            if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
+            if (a.n2 == 2) {  // one A tile + two B slices (N sub-tiles n0, n0 + block_n); bf16 only
+                const uint16_t ow = (uint16_t)(ts * a.dw), oh = (uint16_t)(tr * a.dh);
+                if (CG == 1) {
+                    uint64_t* bar = &full[stage];
+                    mbar_arrive_expect_tx(bar, stage_bytes);
+                    if (a.a_mode == TC_A_IM2COL) tma_load_im2col_4d(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    else tma_load_2d(sA, &ta0, bar, kx, m0);
+                    tma_load_2d(sB, &tb0, bar, kx, n0);
+                    tma_load_2d(sB + b_bytes, &tb0, bar, kx, n0 + a.block_n);
+                } else {
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+                    const uint32_t bar = full_base + stage * 8;
+                    if (a.a_mode == TC_A_IM2COL)
+                        tma_load_im2col_4d_cg2(sA, &ta0, bar, cc * kelems, wbase, hbase, n_img, ow, oh);
+                    else tma_load_2d_cg2(sA, &ta0, bar, kx, m0);
+                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
+                    tma_load_2d_cg2(sB + b_bytes, &tb0, bar, kx, n0 + a.block_n);
+                }
+            } else if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
                 if (leader) mbar_arrive(&full[stage]);
             } else if (CG == 1) {
                 uint64_t* bar = &full[stage];
@@ -294,7 +312,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
     constexpr int splits = CMODE == CM_3XTF32 ? 2 : 1;
     const int bn_cta = a.block_n / CG;
     const uint32_t a_bytes = BM * a.row_bytes, b_bytes = bn_cta * a.row_bytes;
-    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const uint32_t stage_bytes = splits * (a_bytes + a.n2 * b_bytes);
     const uint32_t idesc = make_idesc(BM * CG, a.block_n, CMODE == CM_BF16 ? 1u : 2u);
     const uint32_t s0 = smem_u32(smem);
     const uint64_t a_desc0 = make_sdesc(s0, a.row_bytes);
@@ -312,13 +330,26 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
             if (kc == 0) {
                 TRACE_WAIT(3, mbar_wait(&tempty[acc], acc_phase ^ 1));
                 tc_fence_after();
-                d_tmem = tmem_base + acc * a.block_n;
+                d_tmem = tmem_base + acc * a.block_n * a.n2;
             }
             TRACE_WAIT(2, mbar_wait(&full[stage], phase));
             tc_fence_after();
             const uint64_t soff = (uint64_t)((stage * stage_bytes) >> 4);
             const uint64_t ad = a_desc0 + soff, bd = b_desc0 + soff;
-            if (!no_mma) {
+            if (!no_mma && CMODE == CM_BF16 && a.n2 == 2) {  // same A, B sub-tile +b_bytes, D +block_n
+#pragma unroll
+                for (int k = 0; k < KS; ++k) {
+                    const uint32_t accum = (k > 0 || kc > 0) ? 1u : 0u;
+                    const uint64_t adk = ad + 2 * k, bdk = bd + 2 * k;
+                    if (CG == 2) {
+                        mma_bf16_cg2(d_tmem, adk, bdk, idesc, accum);
+                        mma_bf16_cg2(d_tmem + a.block_n, adk, bdk + blo_off, idesc, accum);
+                    } else {
+                        mma_bf16(d_tmem, adk, bdk, idesc, accum);
+                        mma_bf16(d_tmem + a.block_n, adk, bdk + blo_off, idesc, accum);
+                    }
+                }
+            } else if (!no_mma) {
 #pragma unroll
                 for (int k = 0; k < KS; ++k) {
                     const uint32_t accum = (k > 0 || kc > 0) ? 1u : 0u;
@@ -647,10 +678,13 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                         : (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
     int slot = 0, issued = 0;
     const int n_stg = a.n_stg;
+    // n2 == 1: the two warpgroups take alternate tiles; n2 == 2: both drain every unit, one
+    // N sub-tile each (sub = group)
+    const int sub = a.n2 == 2 ? group : 0;
     int it = -1;
     for (int tile = unit; tile < total_tiles; tile += num_units) {
         ++it;
-        if ((it & 1) != group) continue;
+        if (a.n2 != 2 && (it & 1) != group) continue;
         const int acc = it % a.n_acc;
         const uint32_t acc_phase = (uint32_t)((it / a.n_acc) & 1);
         int n0, row0, qc = 0, img = 0;
@@ -662,12 +696,12 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
         } else {
             const int rem = tile % tiles_per_batch;
             const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
-            n0 = (rem % a.n_tiles) * a.block_n;
+            n0 = ((rem % a.n_tiles) * a.n2 + sub) * a.block_n;
             row0 = m0 + quarter * 32;
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const uint32_t tbase = tmem_base + acc * a.block_n + lane_off;
+        const uint32_t tbase = tmem_base + (acc * a.n2 + sub) * a.block_n + lane_off;
         // 32-column chunks holding real output channels (the last N tile may be partial: its
         // padding columns are never read, and the TMEM release follows the last real chunk)
         const int nvalid = min(ncol32, (a.Ncols - n0 + 31) / 32);
@@ -782,7 +816,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG); }
+        // n2 == 2: both epilogue warpgroups drain every accumulator (one N sub-tile each)
+        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG * a.n2); }
         mbar_init(bres, 1);
         fence_mbar_init();
     }
@@ -868,6 +903,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.store_mode == 1 && a.stg_row != 0 &&
                           (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
+        if (a.n2 == 2 && !fast) __trap();  // N sub-tiles are configured for the fast epilogue only
         if (fast) {
             const uint32_t sb = smem_u32(sbias);
             if (a.a_mode == TC_A_HALO) {
@@ -1170,10 +1206,23 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_BN");  // experiment override: force BLOCK_N
         if (e && atoi(e) > 0) a.block_n = atoi(e);
     }
+    if (a.n2 != 2) a.n2 = 1;  // a re-configure (box64 rows) keeps the first call's choice
     if (a.block_n == 0) {
+        a.n2 = 1;
         const int cg = pick_cg(a.M);
         const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
         a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb);
+        // two N sub-tiles per unit when that makes a multi-wave layer fit in one wave (VGG conv5:
+        // 98 -> 49 units on 74 CTA pairs): each A stage then feeds 2 x block_n columns, and with
+        // one unit per CTA pair the single 512-column TMEM buffer costs no overlap
+        const char* e = getenv("AI3_N2");
+        const bool n2_ok = !(e && e[0] == '0') && a.cm == CM_BF16 && a.batch == 1 &&
+                           (a.a_mode == TC_A_IM2COL || a.a_mode == TC_A_TILED2D) && a.out_bf16 && !a.out_nchw &&
+                           a.stg_row != 0 && a.Ncols <= 2048 && cg == 2 && a.block_n >= 128 &&
+                           a.Ncols % (2 * a.block_n) == 0;
+        const long long groups = num_sms / cg;
+        const long long u1 = m_units * (a.Ncols / a.block_n), u2 = u1 / 2;
+        if (n2_ok && u1 > groups && u2 <= groups) a.n2 = 2;
     }
     // 3xTF32 stages hold four operand tiles; cap the N tile so >= 2 stages fit.
     if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
@@ -1197,6 +1246,7 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_TC_DEBUG");
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
+    if (a.n2 == 2 && (a.store_mode != 1 || !a.epi_fast || a.dbg || a.trace)) a.n2 = 1;  // fast epilogue only
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const bool chunked = a.a_mode == TC_A_HALO && a.halo_chunks > 1;
     if (a.a_mode == TC_A_HALO) {
@@ -1207,7 +1257,8 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.tiles_p = (a.P + a.TP * a.cg - 1) / (a.TP * a.cg);
         a.tiles_q = (a.Q + a.TQ - 1) / a.TQ;
     }
-    const int stage_bytes = a.a_mode == TC_A_HALO ? a.halo_bytes : splits * (BM + a.block_n / a.cg) * a.row_bytes;
+    const int stage_bytes =
+        a.a_mode == TC_A_HALO ? a.halo_bytes : splits * (BM + a.n2 * a.block_n / a.cg) * a.row_bytes;
     if (a.bias_smem && a.Ncols > 2048) a.bias_smem = 0;
     const int fixed = 1024 /* barriers */ + 1024 /* alignment slack */ + (a.bias_smem ? (a.Ncols * 4 + 15) / 16 * 16 : 0) +
                       a.bres_bytes;
@@ -1248,13 +1299,13 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.batch = 1;
     } else {
         a.m_tiles = (a.M + BM * a.cg - 1) / (BM * a.cg);
-        a.n_tiles = (a.Ncols + a.block_n - 1) / a.block_n;
+        a.n_tiles = (a.Ncols + a.block_n * a.n2 - 1) / (a.block_n * a.n2);  // units of n2 N sub-tiles
     }
     p.smem_bytes = chunked ? a.hslots * a.halo_bytes + a.bslots * (a.block_n / a.cg) * 128 + reserve
                            : stages * stage_bytes + reserve;
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
-    a.n_acc = 512 / a.block_n;
+    a.n_acc = 512 / (a.block_n * a.n2);
     if (a.n_acc > MAX_ACC) a.n_acc = MAX_ACC;
     if (a.cm == CM_3XTF32) {
         // 3xTF32: `nch` accumulation chunks per tile; 2 x nch buffers let the two epilogue
@@ -1262,9 +1313,10 @@ void tc_configure(TcPlan& p, int num_sms) {
         const int nch = (a.num_kb + a.promote_kb - 1) / a.promote_kb;
         a.n_acc = 2 * nch <= a.n_acc ? 2 * nch : 2;
     }
-    if (a.n_acc < 2) a.n_acc = 2;
+    if (a.n_acc < 2 && a.n2 == 1) a.n_acc = 2;
+    if (a.n_acc < 1) a.n_acc = 1;  // n2 == 2 at BLOCK_N = 256: one 512-column buffer
     int cols = 32;
-    while (cols < a.n_acc * a.block_n) cols *= 2;
+    while (cols < a.n_acc * a.block_n * a.n2) cols *= 2;
     p.tmem_cols = cols;
     const long long units = (long long)a.m_tiles * a.n_tiles * a.batch;  // one unit = one CTA group's tile
     const int max_units = num_sms / a.cg;
