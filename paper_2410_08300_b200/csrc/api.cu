@@ -172,6 +172,30 @@ ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
     return fail(AI3_ERR_UNKNOWN_ALGORITHM, "unknown algorithm id %d", (int)algo);
 }
 
+// Space-to-depth lowering of implicit_gemm (R24): a strided, undilated conv whose
+// channels cannot fill a 32-byte K-block row (RGB stems: ResNet 7x7 s2, AlexNet 11x11 s4) runs as
+// the stride-1 conv of ceil(R/sh) x ceil(S/sw) taps over the s2d image of sh*sw*C channels.
+bool s2d_eligible(const ConvProblem& c) {
+    const char* e = getenv("AI3_S2D");
+    if (e && e[0] == '0') return false;
+    const int64_t elem = c.dtype == AI3_BF16 ? 2 : 4;
+    return c.G == 1 && c.dh == 1 && c.dw == 1 && (c.sh > 1 || c.sw > 1) && c.C * elem < 32 && c.R >= c.sh &&
+           c.S >= c.sw && c.C * c.sh * c.sw <= 64;
+}
+
+ConvProblem s2d_problem(const ConvProblem& c) {
+    ConvProblem i = c;
+    i.R = (c.R + c.sh - 1) / c.sh;
+    i.S = (c.S + c.sw - 1) / c.sw;
+    i.C = c.C * c.sh * c.sw;
+    i.H = c.P + i.R - 1;
+    i.W = c.Q + i.S - 1;
+    i.sh = i.sw = 1;
+    i.ph = i.pw = 0;
+    i.in_layout = AI3_NHWC;
+    return i;
+}
+
 // The `guess` rule (PAPER.md:190/:200 defer to cuDNN's heuristic).
 // First matching clause wins; deterministic in (shape, params, dtype, math).
 ai3_algo guess_rule(const ConvProblem& c) {
@@ -184,10 +208,13 @@ ai3_algo guess_rule(const ConvProblem& c) {
     if (c.C * (c.dtype == AI3_BF16 ? 2 : 4) < 32) {
         // ...unless the 16-byte-pixel halo mode applies (bf16, C <= 8, stride 1): it gathers
         // all R*S taps from one smem halo per tile with no im2col round trip
-        const bool narrow_halo = c.dtype == AI3_BF16 && c.C <= 8 && c.sh == 1 && c.sw == 1 && c.dh == 1 &&
+        const bool narrow_halo = c.dtype == AI3_BF16 && c.C <= 16 && c.sh == 1 && c.sw == 1 && c.dh == 1 &&
                                  c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 && c.N <= 65535;
         const char* e = getenv("AI3_HALO");
         if (narrow_halo && !(e && e[0] == '0')) return AI3_ALGO_IMPLICIT_GEMM;
+        // ...or the strided conv has a space-to-depth view with full rows
+        if (s2d_eligible(c) && check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
+        g_err.clear();
         return AI3_ALGO_GEMM;
     }
     if (check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
@@ -215,7 +242,9 @@ ai3_status ai3::api_fail(ai3_status st, const char* msg) { return fail(st, "%s",
 
 // ---------------------------------------------------------------- the plan
 struct ai3_plan {
-    ConvProblem pb{};
+    ConvProblem pb{};     // the problem the kernels run (the s2d view when s2d is set)
+    ConvProblem outer{};  // the caller's problem
+    int s2d = 0;          // implicit_gemm over the space-to-depth view (R24)
     ai3_algo algo = AI3_ALGO_DIRECT;
     ComputeMode cm = CM_BF16;
     int elem = 2, splits = 1;
@@ -256,8 +285,16 @@ CUtensorMapSwizzle map_swizzle(int row_bytes) {
                             : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
+ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo);
+
 // Fill sizes / offsets of a plan (no device work).  algo must be resolved.
 ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
+    pl.outer = c;
+    pl.s2d = algo == AI3_ALGO_IMPLICIT_GEMM && s2d_eligible(c) ? 1 : 0;
+    return layout_plan_inner(pl, pl.s2d ? s2d_problem(c) : c, algo);
+}
+
+ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
     if (algo == AI3_ALGO_CUSTOM)
         return fail(AI3_ERR_UNSUPPORTED, "custom algorithms have no plans: run them with ai3_conv2d / ai3_conv2d_custom");
     pl.pb = c;
@@ -281,6 +318,12 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         return ok();
     }
     pl.Cpad = padded_channels(c.C, pl.elem);
+    // s2d views with 33..63 channels (AlexNet conv1: 48): pad to one 64-channel halo chunk
+    // rather than 32-byte im2col rows (AI3_S2D_C64=0 keeps the narrow rows, for A/B)
+    if (pl.s2d && pl.cm == CM_BF16 && pl.Cpad > 32 && pl.Cpad < 64 && c.K <= 128) {
+        const char* e6 = getenv("AI3_S2D_C64");
+        if (!(e6 && e6[0] == '0')) pl.Cpad = 64;
+    }
     pl.Kp = algo == AI3_ALGO_KN2ROW ? pl.Cpad : round_up(c.R * c.S * c.C, 16 / pl.elem);
     // halo modes (implicit GEMM, bf16, stride 1, undilated, K <= 128): 64 channels per pixel
     // (128-byte swizzled rows), or <= 8 channels padded to 8 (16-byte rows, RGB first layers)
@@ -293,6 +336,8 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
                               c.N <= 65535;
         if (allow && shape_ok && pl.Cpad == 64) pl.halo_pb = 128;
         if (allow && shape_ok && c.C <= 8) { pl.halo_pb = 16; pl.Cpad = 8; }
+        // 9..16 channels: 32-byte pixels as two 8-channel planes, one K=16 MMA per tap
+        if (allow && shape_ok && c.C > 8 && c.C <= 16) { pl.halo_pb = 32; pl.Cpad = 16; }
         // chunked halo: 64-channel chunks of wider inputs, weights streamed per (chunk, tap);
         // K <= 128 (measured: VGG conv2_2 238 -> 220 us; at K = 256 the im2col mode was as
         // fast or faster).  AI3_HALO_CHUNKED=0 turns it off (A/B)
@@ -330,7 +375,7 @@ ai3_status layout_plan(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) {
         pl.need_prep = false;  // im2col reads the raw input and writes the operand precision itself
         pl.prep_cm = pl.cm;
     } else {
-        pl.need_prep = pl.cm != CM_BF16 || !nhwc_exact;  // fp32 operands must be rounded / split
+        pl.need_prep = pl.cm != CM_BF16 || !nhwc_exact || pl.s2d;  // fp32 operands must be rounded / split
         pl.prep_cm = pl.cm;
     }
     const size_t xcount = (size_t)c.N * c.H * c.W * pl.Cpad;
@@ -476,7 +521,8 @@ ai3_status encode_b_maps(ai3_plan& pl) {
         const uint64_t kred = (uint64_t)(pl.taps_pad * pl.Cpad);
         const uint64_t dims[2] = {kred, (uint64_t)c.K};
         const uint64_t str[1] = {kred * pl.elem};
-        const uint32_t box[2] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)(a.block_n / a.cg)};
+        const uint32_t box[2] = {(uint32_t)(a.halo_chunks > 1 ? 64 : (a.halo_pb == 128 ? pl.Cpad : 8)),
+                                 (uint32_t)(a.block_n / a.cg)};
         okb = encode_tiled(&pl.tb0, dt, 2, w, dims, str, box,
                            a.halo_pb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
     } else {
@@ -508,6 +554,10 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         if (a.halo_pb == 128) {
             const uint32_t box[4] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)a.RS, (uint32_t)a.HR, 1};
             oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        } else if (a.halo_pb == 32) {
+            // 32-byte pixels: two loads of 8-channel planes (16-byte box rows)
+            const uint32_t box[4] = {8, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+            oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
         } else {
             // 16-byte pixels: view the rows as (W*Cpad, H, N) so that each halo row is one
             // 256-byte box row (left/right padding = out-of-bounds fill on the flat axis)
@@ -600,6 +650,10 @@ ai3_status prepare_weights(ai3_plan& pl, const void* w, const void* bias, cudaSt
                                   reinterpret_cast<float*>(wb + pl.w_off), st);
     } else if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_filter(w, c.dtype, c.K, c.C, pl.Cpad, pl.cm, wb + pl.w_off, wb + pl.wlo_off, st);
+    } else if (pl.s2d) {
+        const ConvProblem& o = pl.outer;
+        e = launch_pack_weights_s2d(w, c.dtype, c.K, o.C, o.R, o.S, o.sh, o.sw, c.R, c.S, pl.taps_pad, pl.Cpad, pl.cm,
+                                    wb + pl.w_off, wb + pl.wlo_off, st);
     } else if (pl.halo_pb) {
         e = launch_pack_weights_taps(w, c.dtype, c.K, c.C, c.R, c.S, pl.taps_pad, pl.Cpad, pl.cm, wb + pl.w_off, st);
     } else if (pl.algo == AI3_ALGO_KN2ROW) {
@@ -648,7 +702,14 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     // 1. input preparation (layout / channel pad / operand precision)
     const void* xs = x;
     const void* xs_lo = nullptr;
-    if (pl.need_prep) {
+    if (pl.s2d) {
+        const ConvProblem& o = pl.outer;
+        e = launch_prep_s2d(x, o.in_layout, o.dtype, o.N, o.C, o.H, o.W, o.sh, o.sw, o.ph, o.pw, c.H, c.W, pl.Cpad,
+                            pl.prep_cm, w + pl.ws_x, w + pl.ws_xlo, st);
+        if (e != cudaSuccess) return cuda_fail(e, "space-to-depth input launch");
+        xs = w + pl.ws_x;
+        xs_lo = w + pl.ws_xlo;
+    } else if (pl.need_prep) {
         e = launch_prep_input(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, pl.Cpad, pl.prep_cm, w + pl.ws_x,
                               w + pl.ws_xlo, st);
         if (e != cudaSuccess) return cuda_fail(e, "input preparation launch");
@@ -867,11 +928,11 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
     if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
     if (!x_host || !y_host || !x_dev || !y_dev) return fail(AI3_ERR_INVALID_ARGUMENT, "null host or staging buffer");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemcpyAsync(x_dev, x_host, act_bytes(plan->pb, false), cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(x_dev, x_host, act_bytes(plan->outer, false), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
     ai3_status s = execute(*plan, x_dev, y_dev, workspace, workspace_bytes, st);
     if (s != AI3_OK) return s;
-    e = cudaMemcpyAsync(y_host, y_dev, act_bytes(plan->pb, true), cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(y_host, y_dev, act_bytes(plan->outer, true), cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy of y");
     return ok();
 }
@@ -910,7 +971,7 @@ ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, cons
     if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, start, 0);
     for (int32_t i = 0; i < n && e == cudaSuccess; ++i) {  // all inputs stream in back to back
-        e = cudaMemcpyAsync(x_devs[i], x_hosts[i], act_bytes(plans[i]->pb, false), cudaMemcpyHostToDevice, h2d);
+        e = cudaMemcpyAsync(x_devs[i], x_hosts[i], act_bytes(plans[i]->outer, false), cudaMemcpyHostToDevice, h2d);
         if (e == cudaSuccess) e = cudaEventRecord(ev[2 * i], h2d);
     }
     for (int32_t i = 0; i < n && e == cudaSuccess && s == AI3_OK; ++i) {
@@ -921,7 +982,7 @@ ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, cons
         e = cudaEventRecord(ev[2 * i + 1], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev[2 * i + 1], 0);  // ...and leaves while i+1 computes
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(y_hosts[i], y_devs[i], act_bytes(plans[i]->pb, true), cudaMemcpyDeviceToHost, d2h);
+            e = cudaMemcpyAsync(y_hosts[i], y_devs[i], act_bytes(plans[i]->outer, true), cudaMemcpyDeviceToHost, d2h);
     }
     if (e == cudaSuccess) e = cudaEventRecord(done, d2h);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, done, 0);  // join: `stream` covers every copy

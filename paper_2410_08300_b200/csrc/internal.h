@@ -42,6 +42,15 @@ struct ConvProblem {
 cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H,
                               int64_t W, int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo,
                               cudaStream_t st);
+// Space-to-depth view of a strided conv (R24): x (NCHW|NHWC, dtype) -> NHWC
+// [N][H2][W2][Cpad], channel (i*sw + u)*C + c = x[c][j*sh - ph + i][l*sw - pw + u] (0 outside), Cpad % 8 == 0.
+cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
+                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, ComputeMode cm,
+                            void* dst, void* dst_lo, cudaStream_t st);
+// KCRS -> [K][taps_pad][Cpad] weights of the space-to-depth conv (T_h x T_w taps), compute mode (+ lo).
+cudaError_t launch_pack_weights_s2d(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S, int sh,
+                                    int sw, int64_t Th, int64_t Tw, int64_t taps_pad, int64_t Cpad, ComputeMode cm,
+                                    void* dst, void* dst_lo, cudaStream_t st);
 // KCRS weights -> [K][R][S][Cpad] in compute mode (+ lo).
 cudaError_t launch_pack_weights(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
                                 int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
@@ -129,7 +138,7 @@ struct TcArgs {
     // TP x TQ output-pixel tile from one (TP+R-1) x RS-slot input halo held in smem; the
     // R*S weight taps stay resident in smem for the whole kernel
     int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
-    int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B) or 16 (<= 8 channels, no swizzle)
+    int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B), 32 (16 channels: two 8-channel planes) or 16 (<= 8 channels), no swizzle below 128
     int taps_pad;   // weight taps held in smem (R*S, rounded up to even for 16-byte pixels)
     // chunked halo (halo_chunks > 1: Cpad = 64 * halo_chunks channels, K <= 256): per tile and
     // 64-channel chunk one halo from a ring of hslots; the weights stream per (chunk, tap)

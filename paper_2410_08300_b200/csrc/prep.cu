@@ -99,6 +99,102 @@ cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- space-to-depth (strided, few channels)
+// A stride-(sh,sw) conv equals a stride-1 conv on the space-to-depth image whose grid starts at the
+// padded origin (-ph,-pw) (R24):
+//   x'[n][j][l][(i*sw + u)*C + c] = x[n][c][j*sh - ph + i][l*sw - pw + u]   (0 outside the image)
+// for j < H', l < W', channel c' < Cpad <= 64 (zero beyond sh*sw*C).  One thread per s2d pixel; the
+// per-channel (row, column, channel) offsets come from a shared-memory table (no per-element division).
+__global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, int64_t N, int C, int H, int W,
+                                int sh, int sw, int ph, int pw, int H2, int W2, int Cpad, int cm, void* dst,
+                                void* dst_lo) {
+    // per s2d channel c': source row / column offset and channel (c' >= sh*sw*C: zero)
+    __shared__ int s_dh[64], s_dw[64], s_c[64];
+    for (int cc = threadIdx.x; cc < Cpad; cc += blockDim.x) {
+        const int ph_idx = cc / C;
+        s_c[cc] = ph_idx < sh * sw ? cc % C : -1;
+        s_dh[cc] = ph_idx / sw - ph;
+        s_dw[cc] = ph_idx % sw - pw;
+    }
+    __syncthreads();
+    const int64_t total = N * H2 * W2;
+    const int64_t plane = (int64_t)H * W;
+    for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < total;
+         pix += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(pix % W2);
+        const int64_t t = pix / W2;
+        const int j = (int)(t % H2);
+        const int64_t n = t / H2;
+        const int64_t img = n * C * plane;
+        for (int g = 0; g < Cpad; g += 8) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int cc = g + e, c = s_c[cc];
+                const int h = j * sh + s_dh[cc], w = l * sw + s_dw[cc];
+                v[e] = 0.f;
+                if (c >= 0 && h >= 0 && h < H && w >= 0 && w < W)
+                    v[e] = load_as_f32(x, img + (nhwc ? ((int64_t)h * W + w) * C + c : c * plane + (int64_t)h * W + w),
+                                       bf16);
+            }
+            const int64_t o = pix * Cpad + g;
+            if (cm == CM_BF16) {
+                __align__(16) __nv_bfloat16 b[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) b[e] = __float2bfloat16_rn(v[e]);
+                *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dst) + o) = *reinterpret_cast<const uint4*>(b);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) store_cm(dst, dst_lo, o + e, v[e], cm);
+            }
+        }
+    }
+}
+
+cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
+                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, ComputeMode cm,
+                            void* dst, void* dst_lo, cudaStream_t st) {
+    if (Cpad % 8 != 0 || Cpad > 64 || H2 > INT32_MAX / 64 || W2 > INT32_MAX / 64)
+        return cudaErrorInvalidValue;
+    const int64_t total = N * H2 * W2;
+    const int64_t blocks = (total + 255) / 256;
+    const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+    prep_s2d_kernel<<<grid, 256, 0, st>>>(x, in_layout == AI3_NHWC, dtype == AI3_BF16, N, (int)C, (int)H, (int)W, sh,
+                                          sw, ph, pw, (int)H2, (int)W2, (int)Cpad, cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
+// KCRS -> [K][taps_pad][Cpad] of the space-to-depth conv: tap (a, b) < (T_h, T_w), channel
+// c' = (i*sw + u)*C + c holds w[k][c][a*sh + i][b*sw + u] (0 beyond R / S, taps >= T_h*T_w, c' >= sh*sw*C).
+__global__ void pack_weights_s2d_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t R,
+                                        int64_t S, int sh, int sw, int64_t Th, int64_t Tw, int64_t taps_pad,
+                                        int64_t Cpad, int cm, void* dst, void* dst_lo) {
+    const int64_t total = K * taps_pad * Cpad;
+    const int64_t Cs = (int64_t)sh * sw * C;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cc = i % Cpad;
+        const int64_t tap = (i / Cpad) % taps_pad;
+        const int64_t k = i / (Cpad * taps_pad);
+        float v = 0.f;
+        if (cc < Cs && tap < Th * Tw) {
+            const int64_t c = cc % C, ph_idx = cc / C;
+            const int64_t r = (tap / Tw) * sh + ph_idx / sw, s = (tap % Tw) * sw + ph_idx % sw;
+            if (r < R && s < S) v = load_as_f32(w, ((k * C + c) * R + r) * S + s, bf16);
+        }
+        store_cm(dst, dst_lo, i, v, cm);
+    }
+}
+
+cudaError_t launch_pack_weights_s2d(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S, int sh,
+                                    int sw, int64_t Th, int64_t Tw, int64_t taps_pad, int64_t Cpad, ComputeMode cm,
+                                    void* dst, void* dst_lo, cudaStream_t st) {
+    const int64_t total = K * taps_pad * Cpad;
+    const int grid = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+    pack_weights_s2d_kernel<<<grid, 256, 0, st>>>(w, dtype == AI3_BF16, K, C, R, S, sh, sw, Th, Tw, taps_pad, Cpad,
+                                                  cm, dst, dst_lo);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- weights
 __global__ void pack_weights_kernel(const void* __restrict__ w, int bf16, int64_t K, int64_t C, int64_t R, int64_t S,
                                     int64_t Cpad, int cm, void* dst, void* dst_lo) {

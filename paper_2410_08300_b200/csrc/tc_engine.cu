@@ -410,14 +410,18 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
     const int n0 = (int)rank * bn_cta;
     const int pb = a.halo_pb, pe = pb / 2;  // bytes / bf16 elements per tap row
     (void)taps;
+    // 32-byte pixels load as two 8-channel planes (rows of 16 B): weights per (tap, plane)
+    const int np = pb == 32 ? 2 : 1, rb = pb / np;
     if (CG == 1) {
         mbar_arrive_expect_tx(bres, (uint32_t)a.bres_bytes);
-        for (int t = 0; t < a.taps_pad; ++t) tma_load_2d(sB + t * bn_cta * pb, &tb0, bres, t * pe, n0);
+        for (int t = 0; t < a.taps_pad * np; ++t) tma_load_2d(sB + t * bn_cta * rb, &tb0, bres, t * (rb / 2), n0);
     } else {
         if (rank == 0) mbar_arrive_expect_tx(bres, 2u * (uint32_t)a.bres_bytes);
         const uint32_t bar = mapa_shared(smem_u32(bres), 0);
-        for (int t = 0; t < a.taps_pad; ++t) tma_load_2d_cg2(sB + t * bn_cta * pb, &tb0, bar, t * pe, n0);
+        for (int t = 0; t < a.taps_pad * np; ++t) tma_load_2d_cg2(sB + t * bn_cta * rb, &tb0, bar, t * (rb / 2), n0);
     }
+    (void)pe;
+    const int plane_bytes = a.HR * a.RS * 16;
     const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
     const int tiles = a.m_tiles;
     int stage = 0;
@@ -433,13 +437,19 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
             mbar_arrive_expect_tx(&full[stage], sm.stage_bytes);
             if (a.halo_pb == 16)  // (W*8, H, N) view: one 256-byte TMA row per halo row
                 tma_load_3d(sA, &ta0, &full[stage], (q0 - a.pw) * 8, p0 - a.ph, n);
-            else
+            else if (a.halo_pb == 32) {  // two 8-channel planes
+                tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
+                tma_load_4d(sA + plane_bytes, &ta0, &full[stage], 8, q0 - a.pw, p0 - a.ph, n);
+            } else
                 tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
         } else {
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sm.stage_bytes);
             if (a.halo_pb == 16)
                 tma_load_3d_cg2(sA, &ta0, full_base + stage * 8, (q0 - a.pw) * 8, p0 - a.ph, n);
-            else
+            else if (a.halo_pb == 32) {
+                tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
+                tma_load_4d_cg2(sA + plane_bytes, &ta0, full_base + stage * 8, 8, q0 - a.pw, p0 - a.ph, n);
+            } else
                 tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
         }
         if (++stage == a.stages) { stage = 0; phase ^= 1; }
@@ -460,12 +470,13 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
     const uint32_t sB = s0 + sm.bres_off;
     const bool no_mma = a.dbg == 1;
     const bool narrow = a.halo_pb == 16;
+    const bool planes2 = a.halo_pb == 32;
     const int RSl = a.RS;  // halo row stride in pixels
     // stage-independent descriptor parts, built once: A at halo offset 0, B per tap
     const uint64_t a0_wide = make_sdesc_sw128(s0, (uint32_t)RSl * 128u, 0u);
     const uint64_t b0_wide = make_sdesc_sw128(sB, 1024u, 0u);
     const uint64_t b0_narrow = make_sdesc_none(sB, (uint32_t)bn_cta * 16u, 128u);
-    const uint32_t b_tap16 = (uint32_t)bn_cta * (narrow ? 16u : 128u) >> 4;  // B tap stride in 16-byte units
+    const uint32_t b_tap16 = (uint32_t)bn_cta * (narrow ? 16u : (planes2 ? 32u : 128u)) >> 4;  // B tap stride (16 B units)
     mbar_wait(bres, 0);
     tc_fence_after();
     int stage = 0, acc = 0;
@@ -477,7 +488,21 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
         TRACE_WAIT(2, mbar_wait(&full[stage], phase));
         tc_fence_after();
         const uint32_t soff16 = (stage * sm.stage_bytes) >> 4;
-        if (!no_mma && narrow) {
+        if (!no_mma && planes2) {
+            // 32-byte pixels as two 8-channel planes, no swizzle: one K=16 slice = one tap;
+            // its second 8 channels sit one plane (LBO) further
+            const uint32_t sbo_n = (uint32_t)RSl * 16u;
+            const uint32_t plane = (uint32_t)(a.HR * RSl * 16);
+            const uint32_t sA = s0 + stage * sm.stage_bytes;
+            const int taps = a.R * a.S;
+            for (int t = 0; t < taps; ++t) {
+                const uint32_t o = (uint32_t)((t / a.S) * RSl + t % a.S) * 16u;
+                const uint64_t ad = make_sdesc_none(sA + o, plane, sbo_n);
+                const uint64_t bd = b0_narrow + (uint64_t)(t * b_tap16);
+                if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, t > 0);
+                else mma_bf16(d_tmem, ad, bd, idesc, t > 0);
+            }
+        } else if (!no_mma && narrow) {
             // 16-byte pixels, no swizzle: one K=16 slice = two filter taps; the second tap's
             // core matrices sit LBO = (its halo offset - the first's) bytes further
             const int taps = a.R * a.S;

@@ -13,6 +13,12 @@ TOL = {("f32", "strict"): 1e-5, ("f32", "tf32"): 1e-3, ("bf16", "strict"): 2e-2,
 WINOGRAD_F32_TOL = 1e-3
 
 
+def stable_seed(key) -> int:
+    """A 16-bit seed from a case key that is the same in every process (hash() of a str is salted)."""
+    import zlib
+    return zlib.crc32(repr(key).encode()) & 0xFFFF
+
+
 def tolerance(algo: str, dtype: str, math: str) -> float:
     if dtype == "f32" and algo == "winograd":
         return WINOGRAD_F32_TOL

@@ -111,6 +111,17 @@ def test_guess_is_deterministic_and_supported(dtype):
             assert a == "direct"
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_guess_strided_rgb_stems_use_s2d_implicit_gemm(dtype):
+    """DESIGN.md R24: strided RGB stems (ResNet 7x7 s2, AlexNet 11x11 s4) have a space-to-depth
+    view with full K-block rows, so guess routes them to implicit_gemm; AI3_S2D=0 restores gemm
+    (checked in a subprocess: the switch is read per call)."""
+    assert ai3.guess((256, 3, 224, 224), 64, 7, 2, 3, 1, 1, dtype=dtype) == "implicit_gemm"
+    assert ai3.guess((128, 3, 224, 224), 64, 11, 4, 2, 1, 1, dtype=dtype) == "implicit_gemm"
+    # a 1x1 strided conv has no s2d benefit (kernel smaller than the stride): explicit GEMM
+    assert ai3.guess((256, 3, 224, 224), 64, 1, 2, 0, 1, 1, dtype=dtype) == "gemm"
+
+
 def test_workspace_sizes():
     lib = _lib.load()
 
