@@ -408,6 +408,15 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.TP = 16; a.TQ = 8; a.RS = 16; a.HR = a.TP + (int)c.R - 1;
         a.halo_pb = pl.halo_pb;
         a.halo_chunks = pl.halo_pb == 128 ? (int)(pl.Cpad / 64) : 1;
+        if (pl.halo_pb == 32) {
+            // NHWC sources load two 8-channel planes (16-byte box rows).  Alternatives, both
+            // parity-green and measured no faster on the ResNet stem: one
+            // SWIZZLE_32B box of whole pixels (AI3_HALO32_SW=1), or plane-split rows written
+            // by the s2d prep, one 256-byte-row box per halo (AI3_S2D_SPLIT=1)
+            const char* e = getenv("AI3_HALO32_SW");
+            const char* es = getenv("AI3_S2D_SPLIT");
+            a.halo32 = pl.s2d && es && es[0] == '1' ? 2 : (e && e[0] == '1' ? 1 : 0);
+        }
         a.taps_pad = (int)pl.taps_pad;
         a.batch_images = (int)c.N;
         {
@@ -555,9 +564,18 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
             const uint32_t box[4] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)a.RS, (uint32_t)a.HR, 1};
             oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
         } else if (a.halo_pb == 32) {
-            // 32-byte pixels: two loads of 8-channel planes (16-byte box rows)
-            const uint32_t box[4] = {8, (uint32_t)a.RS, (uint32_t)a.HR, 1};
-            oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+            // 32-byte pixels: two loads of 8-channel planes (16-byte box rows), or one
+            // SWIZZLE_32B load of whole pixels (AI3_HALO32_SW=1)
+            if (a.halo32 == 2) {
+                const uint64_t d4[4] = {(uint64_t)c.W * 8, 2, (uint64_t)c.H, (uint64_t)c.N};
+                const uint64_t s4[3] = {c.W * 8 * e, c.W * 16 * e, c.H * c.W * 16 * e};
+                const uint32_t box[4] = {(uint32_t)a.RS * 8, 2, (uint32_t)a.HR, 1};
+                oka = encode_tiled(&pl.ta0, dt, 4, src, d4, s4, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+            } else {
+                const uint32_t box[4] = {a.halo32 == 1 ? 16u : 8u, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+                oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box,
+                                   a.halo32 == 1 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+            }
         } else {
             // 16-byte pixels: view the rows as (W*Cpad, H, N) so that each halo row is one
             // 256-byte box row (left/right padding = out-of-bounds fill on the flat axis)
@@ -705,7 +723,8 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if (pl.s2d) {
         const ConvProblem& o = pl.outer;
         e = launch_prep_s2d(x, o.in_layout, o.dtype, o.N, o.C, o.H, o.W, o.sh, o.sw, o.ph, o.pw, c.H, c.W, pl.Cpad,
-                            pl.prep_cm, w + pl.ws_x, w + pl.ws_xlo, st);
+                            pl.tc.args.a_mode == TC_A_HALO && pl.tc.args.halo32 == 2, pl.prep_cm, w + pl.ws_x,
+                            w + pl.ws_xlo, st);
         if (e != cudaSuccess) return cuda_fail(e, "space-to-depth input launch");
         xs = w + pl.ws_x;
         xs_lo = w + pl.ws_xlo;

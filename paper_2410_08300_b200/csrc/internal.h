@@ -44,9 +44,10 @@ cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int
                               cudaStream_t st);
 // Space-to-depth view of a strided conv (R24): x (NCHW|NHWC, dtype) -> NHWC
 // [N][H2][W2][Cpad], channel (i*sw + u)*C + c = x[c][j*sh - ph + i][l*sw - pw + u] (0 outside), Cpad % 8 == 0.
+// split = 1: plane-split rows [N][H2][Cpad/8][W2][8] instead of NHWC (the 32-byte halo's fast source).
 cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
-                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, ComputeMode cm,
-                            void* dst, void* dst_lo, cudaStream_t st);
+                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, int split,
+                            ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
 // KCRS -> [K][taps_pad][Cpad] weights of the space-to-depth conv (T_h x T_w taps), compute mode (+ lo).
 cudaError_t launch_pack_weights_s2d(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S, int sh,
                                     int sw, int64_t Th, int64_t Tw, int64_t taps_pad, int64_t Cpad, ComputeMode cm,
@@ -139,6 +140,8 @@ struct TcArgs {
     // R*S weight taps stay resident in smem for the whole kernel
     int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
     int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B), 32 (16 channels: two 8-channel planes) or 16 (<= 8 channels), no swizzle below 128
+    int halo32;     // halo_pb == 32 source: 0 = NHWC pixels, two 8-channel plane loads; 1 = NHWC pixels, one
+                    // SWIZZLE_32B load; 2 = plane-split rows [n][h][2][w][8] (s2d prep), one 256-byte-row load
     int taps_pad;   // weight taps held in smem (R*S, rounded up to even for 16-byte pixels)
     // chunked halo (halo_chunks > 1: Cpad = 64 * halo_chunks channels, K <= 256): per tile and
     // 64-channel chunk one halo from a ring of hslots; the weights stream per (chunk, tap)

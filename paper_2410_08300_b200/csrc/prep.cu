@@ -106,8 +106,8 @@ cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int
 // for j < H', l < W', channel c' < Cpad <= 64 (zero beyond sh*sw*C).  One thread per s2d pixel; the
 // per-channel (row, column, channel) offsets come from a shared-memory table (no per-element division).
 __global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, int64_t N, int C, int H, int W,
-                                int sh, int sw, int ph, int pw, int H2, int W2, int Cpad, int cm, void* dst,
-                                void* dst_lo) {
+                                int sh, int sw, int ph, int pw, int H2, int W2, int Cpad, int split, int cm,
+                                void* dst, void* dst_lo) {
     // per s2d channel c': source row / column offset and channel (c' >= sh*sw*C: zero)
     __shared__ int s_dh[64], s_dw[64], s_c[64];
     for (int cc = threadIdx.x; cc < Cpad; cc += blockDim.x) {
@@ -137,7 +137,8 @@ __global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, 
                     v[e] = load_as_f32(x, img + (nhwc ? ((int64_t)h * W + w) * C + c : c * plane + (int64_t)h * W + w),
                                        bf16);
             }
-            const int64_t o = pix * Cpad + g;
+            // NHWC, or plane-split rows: ((n*H2 + j)*(Cpad/8) + g/8)*W2*8 + l*8
+            const int64_t o = split ? (t * (Cpad / 8) + g / 8) * (int64_t)W2 * 8 + (int64_t)l * 8 : pix * Cpad + g;
             if (cm == CM_BF16) {
                 __align__(16) __nv_bfloat16 b[8];
 #pragma unroll
@@ -152,15 +153,15 @@ __global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, 
 }
 
 cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
-                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, ComputeMode cm,
-                            void* dst, void* dst_lo, cudaStream_t st) {
+                            int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, int split,
+                            ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
     if (Cpad % 8 != 0 || Cpad > 64 || H2 > INT32_MAX / 64 || W2 > INT32_MAX / 64)
         return cudaErrorInvalidValue;
     const int64_t total = N * H2 * W2;
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
     prep_s2d_kernel<<<grid, 256, 0, st>>>(x, in_layout == AI3_NHWC, dtype == AI3_BF16, N, (int)C, (int)H, (int)W, sh,
-                                          sw, ph, pw, (int)H2, (int)W2, (int)Cpad, cm, dst, dst_lo);
+                                          sw, ph, pw, (int)H2, (int)W2, (int)Cpad, split, cm, dst, dst_lo);
     return cudaGetLastError();
 }
 

@@ -394,6 +394,17 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t sb
     d |= 2ull << 61;
     return d;
 }
+// K-major SWIZZLE_32B descriptor (32-byte rows = one K=16 bf16 slice), 8-row groups `sbo` apart;
+// the start may sit at any 32-byte row (the swizzle applies to absolute address bits).
+__device__ __forceinline__ uint64_t make_sdesc_sw32(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;
+    d |= 6ull << 61;
+    return d;
+}
 }  // namespace ai3
 
 namespace ai3 {

@@ -437,7 +437,9 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
             mbar_arrive_expect_tx(&full[stage], sm.stage_bytes);
             if (a.halo_pb == 16)  // (W*8, H, N) view: one 256-byte TMA row per halo row
                 tma_load_3d(sA, &ta0, &full[stage], (q0 - a.pw) * 8, p0 - a.ph, n);
-            else if (a.halo_pb == 32) {  // two 8-channel planes
+            else if (a.halo_pb == 32 && a.halo32 == 2)  // plane-split rows: (W*8, 2, H, N) view
+                tma_load_4d(sA, &ta0, &full[stage], (q0 - a.pw) * 8, 0, p0 - a.ph, n);
+            else if (a.halo_pb == 32 && a.halo32 == 0) {  // two 8-channel planes
                 tma_load_4d(sA, &ta0, &full[stage], 0, q0 - a.pw, p0 - a.ph, n);
                 tma_load_4d(sA + plane_bytes, &ta0, &full[stage], 8, q0 - a.pw, p0 - a.ph, n);
             } else
@@ -446,7 +448,9 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * sm.stage_bytes);
             if (a.halo_pb == 16)
                 tma_load_3d_cg2(sA, &ta0, full_base + stage * 8, (q0 - a.pw) * 8, p0 - a.ph, n);
-            else if (a.halo_pb == 32) {
+            else if (a.halo_pb == 32 && a.halo32 == 2)
+                tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, (q0 - a.pw) * 8, 0, p0 - a.ph, n);
+            else if (a.halo_pb == 32 && a.halo32 == 0) {
                 tma_load_4d_cg2(sA, &ta0, full_base + stage * 8, 0, q0 - a.pw, p0 - a.ph, n);
                 tma_load_4d_cg2(sA + plane_bytes, &ta0, full_base + stage * 8, 8, q0 - a.pw, p0 - a.ph, n);
             } else
@@ -496,8 +500,14 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
             const uint32_t sA = s0 + stage * sm.stage_bytes;
             const int taps = a.R * a.S;
             for (int t = 0; t < taps; ++t) {
-                const uint32_t o = (uint32_t)((t / a.S) * RSl + t % a.S) * 16u;
-                const uint64_t ad = make_sdesc_none(sA + o, plane, sbo_n);
+                const uint32_t px = (uint32_t)((t / a.S) * RSl + t % a.S);
+                // halo32 == 2: smem [HR][2][RS][8]: tap (r, s) at (r*2*RS + s)*16 B, plane 1 RS*16 B
+                // further (LBO), next output row 2*RS*16 B (SBO)
+                const uint64_t ad =
+                    a.halo32 == 1 ? make_sdesc_sw32(sA + px * 32u, sbo_n * 2u)
+                    : a.halo32 == 2
+                        ? make_sdesc_none(sA + (uint32_t)((t / a.S) * 2 * RSl + t % a.S) * 16u, sbo_n, sbo_n * 2u)
+                        : make_sdesc_none(sA + px * 16u, plane, sbo_n);
                 const uint64_t bd = b0_narrow + (uint64_t)(t * b_tap16);
                 if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, t > 0);
                 else mma_bf16(d_tmem, ad, bd, idesc, t > 0);
