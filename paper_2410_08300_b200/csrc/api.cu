@@ -409,13 +409,13 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.halo_pb = pl.halo_pb;
         a.halo_chunks = pl.halo_pb == 128 ? (int)(pl.Cpad / 64) : 1;
         if (pl.halo_pb == 32) {
-            // NHWC sources load two 8-channel planes (16-byte box rows).  Alternatives, both
-            // parity-green and measured no faster on the ResNet stem: one
-            // SWIZZLE_32B box of whole pixels (AI3_HALO32_SW=1), or plane-split rows written
-            // by the s2d prep, one 256-byte-row box per halo (AI3_S2D_SPLIT=1)
+            // s2d views: the prep writes plane-split rows, loaded as one 256-byte-row box per halo
+            // (AI3_S2D_SPLIT=0: NHWC).  NHWC sources: two 8-channel planes (16-byte box rows), or
+            // one SWIZZLE_32B box of whole pixels (AI3_HALO32_SW=1).  Same-box, ResNet stem:
+            // 220 / 231 / 224 us
             const char* e = getenv("AI3_HALO32_SW");
             const char* es = getenv("AI3_S2D_SPLIT");
-            a.halo32 = pl.s2d && es && es[0] == '1' ? 2 : (e && e[0] == '1' ? 1 : 0);
+            a.halo32 = pl.s2d && !(es && es[0] == '0') ? 2 : (e && e[0] == '1' ? 1 : 0);
         }
         a.taps_pad = (int)pl.taps_pad;
         a.batch_images = (int)c.N;

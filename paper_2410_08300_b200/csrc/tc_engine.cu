@@ -499,18 +499,23 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
             const uint32_t plane = (uint32_t)(a.HR * RSl * 16);
             const uint32_t sA = s0 + stage * sm.stage_bytes;
             const int taps = a.R * a.S;
+            // descriptor of tap (r, s) = base + (r*row + s) * step (16-byte units), built per layout:
+            //  0: two planes, pixels 16 B apart, plane 1 at LBO = plane, rows SBO = RS*16;
+            //  1: SWIZZLE_32B whole pixels, 32 B apart, rows SBO = RS*32;
+            //  2: plane-split rows [HR][2][RS][8]: plane 1 at LBO = RS*16, rows SBO = 2*RS*16
+            const int mode = a.halo32;
+            const uint64_t ad0 = mode == 1 ? make_sdesc_sw32(sA, sbo_n * 2u)
+                                 : mode == 2 ? make_sdesc_none(sA, sbo_n, sbo_n * 2u)
+                                             : make_sdesc_none(sA, plane, sbo_n);
+            const uint32_t row16 = (uint32_t)RSl * (mode == 0 ? 1u : 2u);  // halo row, 16-byte units
+            const uint32_t px16 = mode == 1 ? 2u : 1u;                       // pixel step, 16-byte units
+            int r = 0, s = 0;
             for (int t = 0; t < taps; ++t) {
-                const uint32_t px = (uint32_t)((t / a.S) * RSl + t % a.S);
-                // halo32 == 2: smem [HR][2][RS][8]: tap (r, s) at (r*2*RS + s)*16 B, plane 1 RS*16 B
-                // further (LBO), next output row 2*RS*16 B (SBO)
-                const uint64_t ad =
-                    a.halo32 == 1 ? make_sdesc_sw32(sA + px * 32u, sbo_n * 2u)
-                    : a.halo32 == 2
-                        ? make_sdesc_none(sA + (uint32_t)((t / a.S) * 2 * RSl + t % a.S) * 16u, sbo_n, sbo_n * 2u)
-                        : make_sdesc_none(sA + px * 16u, plane, sbo_n);
+                const uint64_t ad = ad0 + (uint64_t)((uint32_t)r * row16 + (uint32_t)s * px16);
                 const uint64_t bd = b0_narrow + (uint64_t)(t * b_tap16);
                 if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, t > 0);
                 else mma_bf16(d_tmem, ad, bd, idesc, t > 0);
+                if (++s == a.S) { s = 0; ++r; }
             }
         } else if (!no_mma && narrow) {
             // 16-byte pixels, no swizzle: one K=16 slice = two filter taps; the second tap's
@@ -530,14 +535,21 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
                     else mma_bf16(d_tmem, ad, bd, idesc, j > 0);
                 }
             } else {
+                // (row, column) of taps t0 = 2j and t1 = 2j + 1 advanced incrementally: no integer
+                // division in the single-thread issue loop (measured: it throttles short MMAs)
+                int r0 = 0, c0 = 0;
                 for (int j = 0; j < a.taps_pad / 2; ++j) {
                     const int t0 = 2 * j, t1 = 2 * j + 1;
-                    const uint32_t o0 = (uint32_t)((t0 / a.S) * RSl + t0 % a.S) * 16u;
-                    const uint32_t o1 = t1 < taps ? (uint32_t)((t1 / a.S) * RSl + t1 % a.S) * 16u : o0 + 16u;
+                    int r1 = r0, c1 = c0 + 1;
+                    if (c1 == a.S) { c1 = 0; ++r1; }
+                    const uint32_t o0 = (uint32_t)(r0 * RSl + c0) * 16u;
+                    const uint32_t o1 = t1 < taps ? (uint32_t)(r1 * RSl + c1) * 16u : o0 + 16u;
                     const uint64_t ad = make_sdesc_none(sA + o0, o1 - o0, sbo_n);
                     const uint64_t bd = b0_narrow + (uint64_t)(t0 * b_tap16);
                     if (CG == 2) mma_bf16_cg2(d_tmem, ad, bd, idesc, j > 0);
                     else mma_bf16(d_tmem, ad, bd, idesc, j > 0);
+                    r0 = r1; c0 = c1 + 1;
+                    if (c0 == a.S) { c0 = 0; ++r0; }
                 }
             }
         } else if (!no_mma) {
