@@ -245,6 +245,7 @@ struct ai3_plan {
     ConvProblem pb{};     // the problem the kernels run (the s2d view when s2d is set)
     ConvProblem outer{};  // the caller's problem
     int s2d = 0;          // implicit_gemm over the space-to-depth view (R24)
+    int flat = 0;         // implicit_gemm of a 1x1 / stride-1 / unpadded conv: A is the NHWC input itself
     ai3_algo algo = AI3_ALGO_DIRECT;
     ComputeMode cm = CM_BF16;
     int elem = 2, splits = 1;
@@ -434,6 +435,16 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.num_kb = (int)(c.R * c.S * a.c_chunks);
         a.gather_rows = (int)pl.idx_rows;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
+    } else if (algo == AI3_ALGO_IMPLICIT_GEMM && c.R == 1 && c.S == 1 && c.sh == 1 && c.sw == 1 && c.ph == 0 &&
+               c.pw == 0 && !(getenv("AI3_FLAT1X1") && getenv("AI3_FLAT1X1")[0] == '0')) {
+        // 1x1, stride 1, no padding: the A operand is the NHWC input [N*H*W][Cpad] itself, loaded
+        // with plain tiled TMA boxes (no im2col traversal)
+        pl.flat = 1;
+        a.a_mode = TC_A_TILED2D;
+        a.M = (int)M;
+        a.row_bytes = implicit_row_bytes(pl.Cpad, pl.elem);
+        a.num_kb = (int)(pl.Cpad * pl.elem / a.row_bytes);
+        pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_GEMM) {
         a.a_mode = TC_A_IM2COL;
         a.M = (int)M;
@@ -584,6 +595,12 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
             const uint32_t box[3] = {(uint32_t)(a.RS * pl.Cpad), (uint32_t)a.HR, 1};
             oka = encode_tiled(&pl.ta0, dt, 3, src, d3, s3, box, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
+    } else if (pl.flat) {
+        const uint64_t dims[2] = {(uint64_t)pl.Cpad, (uint64_t)a.M};
+        const uint64_t str[1] = {(uint64_t)pl.Cpad * e};
+        const uint32_t box[2] = {kel, 128};
+        oka = encode_tiled(&pl.ta0, dt, 2, src, dims, str, box, sw);
+        if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 2, src_lo, dims, str, box, sw);
     } else if (pl.algo == AI3_ALGO_IMPLICIT_GEMM) {
         const uint64_t dims[4] = {(uint64_t)pl.Cpad, (uint64_t)c.W, (uint64_t)c.H, (uint64_t)c.N};
         const uint64_t str[3] = {pl.Cpad * e, c.W * pl.Cpad * e, c.H * c.W * pl.Cpad * e};

@@ -11,7 +11,7 @@ net = sys.argv[2] if len(sys.argv) > 2 else "vgg16"
 spec = [l for l in workload(net) if l.name == sys.argv[1]][0]
 x = torch.randn(spec.N, spec.C, spec.H, spec.W, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
 _, w, b = conv_inputs(spec.with_batch(1), 1, "bf16")
-p = ai3.ConvPlan(torch.from_numpy(w).cuda().bfloat16(), torch.from_numpy(b).cuda().bfloat16(), x.shape, spec.stride,
+p = ai3.ConvPlan(torch.from_numpy(w).cuda().bfloat16(), None if b is None else torch.from_numpy(b).cuda().bfloat16(), x.shape, spec.stride,
                  spec.pad, spec.dil, 1, sys.argv[3] if len(sys.argv) > 3 else "guess", in_layout=1)
 y = p(x); torch.cuda.synchronize()
 lib = _lib.load()
