@@ -332,7 +332,11 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     {
         const char* e = getenv("AI3_HALO");
         const bool allow = !(e && e[0] == '0');
-        const bool shape_ok = algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
+        // 1x1 convs take the flat mode below (a halo of a 1x1 filter is just the tile, and the
+        // 16x8-pixel halo tiles pad 28x28 / 14x14 maps); AI3_HALO1X1=1 keeps them in halo mode (A/B)
+        const char* e1 = getenv("AI3_HALO1X1");
+        const bool not1x1 = !(c.R == 1 && c.S == 1) || (e1 && e1[0] == '1');
+        const bool shape_ok = not1x1 && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
                               c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
                               c.N <= 65535;
         if (allow && shape_ok && pl.Cpad == 64) pl.halo_pb = 128;
@@ -344,7 +348,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         // fast or faster).  AI3_HALO_CHUNKED=0 turns it off (A/B)
         const char* ec = getenv("AI3_HALO_CHUNKED");
         const bool allow_c = allow && !(ec && ec[0] == '0');
-        const bool shape_c = algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
+        const bool shape_c = not1x1 && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
                              c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
                              c.N <= 65535 && pl.Cpad % 64 == 0 && pl.Cpad >= 128;
         if (allow_c && shape_c) pl.halo_pb = 128;

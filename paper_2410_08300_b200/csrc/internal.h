@@ -156,6 +156,7 @@ struct TcArgs {
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
     int relu;       // 1: fused ReLU after the bias (model path)
+    int pf_tiles;   // TILED2D: prefetch the A panel of the tile this many scheduler steps ahead into L2 (0 = off)
     int n2;         // N sub-tiles per unit (1, or 2: one A stage feeds two block_n-column MMAs --
                     // for single-wave layers; bf16 im2col / tiled with the fast epilogue only)
     // gather mode (a_mode == TC_A_GATHER, implicit_precomp_gemm): precomputed input-row table

@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 #include <cstdlib>
 #include <mutex>
+#include <cstdio>
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -154,6 +155,15 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
             const int p = pq / a.Q;
             hbase = p * a.sh - a.ph;
             wbase = (pq - p * a.Q) * a.sw - a.pw;
+        }
+        if (a.pf_tiles > 0 && a.a_mode == TC_A_TILED2D && a.batch == 1) {
+            // streaming layers (1x1 convs reading their input once): the A panel of a later
+            // tile is prefetched into L2 so that more HBM reads are in flight than the stage ring holds
+            const int tpf = tile + a.pf_tiles * num_units;
+            if (tpf < total_tiles && (tpf % a.n_tiles) == 0) {
+                const int m_pf = (tpf / a.n_tiles) * (BM * CG) + (int)rank * BM;
+                for (int kb = 0; kb < a.num_kb; ++kb) tma_prefetch_l2_2d(&ta0, kb * kelems, m_pf);
+            }
         }
         int cc = 0, ts = 0, tr = 0;  // channel chunk, filter column, filter row of the current K-block
         for (int kb = 0; kb < a.num_kb; ++kb) {
@@ -1294,6 +1304,10 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
     if (a.n2 == 2 && (a.store_mode != 1 || !a.epi_fast || a.dbg || a.trace)) a.n2 = 1;  // fast epilogue only
+    {
+        const char* e = getenv("AI3_PF");  // L2 prefetch distance in scheduler steps (TILED2D)
+        a.pf_tiles = (e && e[0] >= '0' && e[0] <= '9') ? atoi(e) : 0;
+    }
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const bool chunked = a.a_mode == TC_A_HALO && a.halo_chunks > 1;
     if (a.a_mode == TC_A_HALO) {
@@ -1369,6 +1383,13 @@ void tc_configure(TcPlan& p, int num_sms) {
     const int max_units = num_sms / a.cg;
     p.grid = (int)(units < max_units ? units : max_units) * a.cg;
     if (p.grid < a.cg) p.grid = a.cg;
+    if (getenv("AI3_TC_VERBOSE")) {  // configuration dump for A/B work (stderr)
+        fprintf(stderr,
+                "[ai3 tc] mode=%d M=%d N=%d bn=%d cg=%d n2=%d row=%d kb=%d stages=%d n_stg=%d stg_row=%d box64=%d "
+                "n_acc=%d m_tiles=%d n_tiles=%d grid=%d smem=%d\n",
+                a.a_mode, a.M, a.Ncols, a.block_n, a.cg, a.n2, a.row_bytes, a.num_kb, a.stages, a.n_stg, a.stg_row,
+                a.box64, a.n_acc, a.m_tiles, a.n_tiles, p.grid, p.smem_bytes);
+    }
 }
 
 cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b0,
