@@ -73,6 +73,7 @@ class ClockSampler(threading.Thread):
         self.index = index
         self.samples, self.max_mhz, self.reasons = [], None, set()
         self._stop_evt = threading.Event()
+        self.ready = threading.Event()  # NVML initialised and sampling (nvmlInit can take > 100 ms)
         self.ok = False
 
     def run(self):
@@ -91,9 +92,17 @@ class ClockSampler(threading.Thread):
                 for bit, name in self.REASONS.items():
                     if mask & bit and name != "gpu_idle":
                         self.reasons.add(name)
-                time.sleep(0.01)
+                self.ready.set()
+                time.sleep(0.005)
         except Exception:
             self.ok = False
+            self.ready.set()
+
+    def begin(self):
+        """Wait until sampling runs, then keep only samples from the timed region on."""
+        self.ready.wait(timeout=20)
+        self.samples.clear()
+        self.reasons.clear()
 
     def stop(self):
         self._stop_evt.set()
@@ -226,7 +235,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     sampler = ClockSampler(device.index if device.index is not None else 0)
     sampler.start()
-    time.sleep(0.05)
+    sampler.begin()
     if dist:
         dist.barrier()
     torch.cuda.synchronize(device)
