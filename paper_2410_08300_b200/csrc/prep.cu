@@ -105,7 +105,8 @@ cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int
 //   x'[n][j][l][(i*sw + u)*C + c] = x[n][c][j*sh - ph + i][l*sw - pw + u]   (0 outside the image)
 // for j < H', l < W', channel c' < Cpad <= 64 (zero beyond sh*sw*C).  One thread per s2d pixel; the
 // per-channel (row, column, channel) offsets come from a shared-memory table (no per-element division).
-__global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, int64_t N, int C, int H, int W,
+template <int NHWC, int BF16>
+__global__ void prep_s2d_kernel(const void* __restrict__ x, int64_t N, int C, int H, int W,
                                 int sh, int sw, int ph, int pw, int H2, int W2, int Cpad, int split, int cm,
                                 void* dst, void* dst_lo) {
     // per s2d channel c': source row / column offset and channel (c' >= sh*sw*C: zero)
@@ -133,9 +134,11 @@ __global__ void prep_s2d_kernel(const void* __restrict__ x, int nhwc, int bf16, 
                 const int cc = g + e, c = s_c[cc];
                 const int h = j * sh + s_dh[cc], w = l * sw + s_dw[cc];
                 v[e] = 0.f;
-                if (c >= 0 && h >= 0 && h < H && w >= 0 && w < W)
-                    v[e] = load_as_f32(x, img + (nhwc ? ((int64_t)h * W + w) * C + c : c * plane + (int64_t)h * W + w),
-                                       bf16);
+                if (c >= 0 && h >= 0 && h < H && w >= 0 && w < W) {
+                    const int64_t i = img + (NHWC ? ((int64_t)h * W + w) * C + c : c * plane + (int64_t)h * W + w);
+                    v[e] = BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[i])
+                                : reinterpret_cast<const float*>(x)[i];
+                }
             }
             // NHWC, or plane-split rows: ((n*H2 + j)*(Cpad/8) + g/8)*W2*8 + l*8
             const int64_t o = split ? (t * (Cpad / 8) + g / 8) * (int64_t)W2 * 8 + (int64_t)l * 8 : pix * Cpad + g;
@@ -160,8 +163,10 @@ cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64
     const int64_t total = N * H2 * W2;
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-    prep_s2d_kernel<<<grid, 256, 0, st>>>(x, in_layout == AI3_NHWC, dtype == AI3_BF16, N, (int)C, (int)H, (int)W, sh,
-                                          sw, ph, pw, (int)H2, (int)W2, (int)Cpad, split, cm, dst, dst_lo);
+    auto k = in_layout == AI3_NHWC ? (dtype == AI3_BF16 ? prep_s2d_kernel<1, 1> : prep_s2d_kernel<1, 0>)
+                                   : (dtype == AI3_BF16 ? prep_s2d_kernel<0, 1> : prep_s2d_kernel<0, 0>);
+    k<<<grid, 256, 0, st>>>(x, N, (int)C, (int)H, (int)W, sh, sw, ph, pw, (int)H2, (int)W2, (int)Cpad, split, cm, dst,
+                            dst_lo);
     return cudaGetLastError();
 }
 
