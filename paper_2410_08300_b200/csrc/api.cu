@@ -180,7 +180,7 @@ bool s2d_eligible(const ConvProblem& c) {
     if (e && e[0] == '0') return false;
     const int64_t elem = c.dtype == AI3_BF16 ? 2 : 4;
     return c.G == 1 && c.dh == 1 && c.dw == 1 && (c.sh > 1 || c.sw > 1) && c.C * elem < 32 && c.R >= c.sh &&
-           c.S >= c.sw && c.C * c.sh * c.sw <= 64;
+           c.S >= c.sw && c.C * c.sh * c.sw <= 64 && c.H * c.W * c.C < INT32_MAX;  // prep: 32-bit in-image offsets
 }
 
 ConvProblem s2d_problem(const ConvProblem& c) {

@@ -105,43 +105,49 @@ cudaError_t launch_prep_input(const void* x, int in_layout, ai3_dtype dtype, int
 //   x'[n][j][l][(i*sw + u)*C + c] = x[n][c][j*sh - ph + i][l*sw - pw + u]   (0 outside the image)
 // for j < H', l < W', channel c' < Cpad <= 64 (zero beyond sh*sw*C).  One thread per s2d pixel; the
 // per-channel (row, column, channel) offsets come from a shared-memory table (no per-element division).
-template <int NHWC, int BF16>
+template <int NHWC, int BF16, typename IDX>  // IDX: uint32_t when every pixel / element index fits, else int64_t
 __global__ void prep_s2d_kernel(const void* __restrict__ x, int64_t N, int C, int H, int W,
                                 int sh, int sw, int ph, int pw, int H2, int W2, int Cpad, int split, int cm,
                                 void* dst, void* dst_lo) {
-    // per s2d channel c': source row / column offset and channel (c' >= sh*sw*C: zero)
-    __shared__ int s_dh[64], s_dw[64], s_c[64];
+    // per s2d channel c': {source channel (-1: zero), row offset, column offset, in-image channel offset}
+    __shared__ int4 s_tab[64];
     for (int cc = threadIdx.x; cc < Cpad; cc += blockDim.x) {
-        const int ph_idx = cc / C;
-        s_c[cc] = ph_idx < sh * sw ? cc % C : -1;
-        s_dh[cc] = ph_idx / sw - ph;
-        s_dw[cc] = ph_idx % sw - pw;
+        const int ph_idx = cc / C, c = cc % C;
+        s_tab[cc] = make_int4(ph_idx < sh * sw ? c : -1, ph_idx / sw - ph, ph_idx % sw - pw, NHWC ? c : c * H * W);
     }
     __syncthreads();
-    const int64_t total = N * H2 * W2;
-    const int64_t plane = (int64_t)H * W;
-    for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < total;
-         pix += (int64_t)gridDim.x * blockDim.x) {
-        const int l = (int)(pix % W2);
-        const int64_t t = pix / W2;
-        const int j = (int)(t % H2);
-        const int64_t n = t / H2;
-        const int64_t img = n * C * plane;
-        for (int g = 0; g < Cpad; g += 8) {
+    // one thread per (s2d pixel, run of GPT 8-channel groups): wide s2d pixels (AlexNet: 64
+    // channels) spread over several threads so that the grid covers the machine
+    const int GPT = Cpad / 8;  // measured: splitting AlexNet's 64-channel pixels over 4 threads was slower (76 -> 101 us)
+    const int runs = Cpad / 8 / GPT;
+    const IDX total = (IDX)(N * H2 * W2) * (IDX)runs;
+    const IDX img_elems = (IDX)H * W * C;
+    const int pstride = NHWC ? C : 1;  // elements between horizontally adjacent pixels
+    for (IDX item = blockIdx.x * (IDX)blockDim.x + threadIdx.x; item < total; item += (IDX)gridDim.x * blockDim.x) {
+        const IDX pix = item / (IDX)runs;
+        const int g0 = (int)(item - pix * (IDX)runs) * GPT * 8;
+        const int l = (int)(pix % (IDX)W2);
+        const IDX t = pix / (IDX)W2;
+        const int j = (int)(t % (IDX)H2);
+        const IDX n = t / (IDX)H2;
+        const IDX img = n * img_elems;
+        const int hb = j * sh, wb = l * sw;
+        for (int g = g0; g < g0 + GPT * 8; g += 8) {
             float v[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const int cc = g + e, c = s_c[cc];
-                const int h = j * sh + s_dh[cc], w = l * sw + s_dw[cc];
+                const int4 tb = s_tab[g + e];
+                const int h = hb + tb.y, w = wb + tb.z;
                 v[e] = 0.f;
-                if (c >= 0 && h >= 0 && h < H && w >= 0 && w < W) {
-                    const int64_t i = img + (NHWC ? ((int64_t)h * W + w) * C + c : c * plane + (int64_t)h * W + w);
+                if (tb.x >= 0 && (unsigned)h < (unsigned)H && (unsigned)w < (unsigned)W) {
+                    const IDX i = img + (IDX)((h * W + w) * pstride + tb.w);
                     v[e] = BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(x)[i])
                                 : reinterpret_cast<const float*>(x)[i];
                 }
             }
             // NHWC, or plane-split rows: ((n*H2 + j)*(Cpad/8) + g/8)*W2*8 + l*8
-            const int64_t o = split ? (t * (Cpad / 8) + g / 8) * (int64_t)W2 * 8 + (int64_t)l * 8 : pix * Cpad + g;
+            const int64_t o = split ? ((int64_t)t * (Cpad / 8) + g / 8) * (int64_t)W2 * 8 + (int64_t)l * 8
+                                    : (int64_t)pix * Cpad + g;
             if (cm == CM_BF16) {
                 __align__(16) __nv_bfloat16 b[8];
 #pragma unroll
@@ -158,13 +164,18 @@ __global__ void prep_s2d_kernel(const void* __restrict__ x, int64_t N, int C, in
 cudaError_t launch_prep_s2d(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
                             int sh, int sw, int ph, int pw, int64_t H2, int64_t W2, int64_t Cpad, int split,
                             ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st) {
-    if (Cpad % 8 != 0 || Cpad > 64 || H2 > INT32_MAX / 64 || W2 > INT32_MAX / 64)
+    if (Cpad % 8 != 0 || Cpad > 64 || H2 > INT32_MAX / 64 || W2 > INT32_MAX / 64 || H * W * C >= INT32_MAX)
         return cudaErrorInvalidValue;
-    const int64_t total = N * H2 * W2;
+    const int64_t total = N * H2 * W2 * (Cpad / 8);  // upper bound of the kernel's (pixel, run) items
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-    auto k = in_layout == AI3_NHWC ? (dtype == AI3_BF16 ? prep_s2d_kernel<1, 1> : prep_s2d_kernel<1, 0>)
-                                   : (dtype == AI3_BF16 ? prep_s2d_kernel<0, 1> : prep_s2d_kernel<0, 0>);
+    // 32-bit index math when the input and the s2d pixel count fit (one image's offsets always do)
+    const bool narrow = N * H * W * C < (int64_t)UINT32_MAX && N * H2 * W2 * (Cpad / 8) + 148 * 16 * 256 < (int64_t)UINT32_MAX;
+    auto k = in_layout == AI3_NHWC
+                 ? (dtype == AI3_BF16 ? (narrow ? prep_s2d_kernel<1, 1, uint32_t> : prep_s2d_kernel<1, 1, int64_t>)
+                                      : (narrow ? prep_s2d_kernel<1, 0, uint32_t> : prep_s2d_kernel<1, 0, int64_t>))
+                 : (dtype == AI3_BF16 ? (narrow ? prep_s2d_kernel<0, 1, uint32_t> : prep_s2d_kernel<0, 1, int64_t>)
+                                      : (narrow ? prep_s2d_kernel<0, 0, uint32_t> : prep_s2d_kernel<0, 0, int64_t>));
     k<<<grid, 256, 0, st>>>(x, N, (int)C, (int)H, (int)W, sh, sw, ph, pw, (int)H2, (int)W2, (int)Cpad, split, cm, dst,
                             dst_lo);
     return cudaGetLastError();
