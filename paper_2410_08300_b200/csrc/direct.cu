@@ -15,6 +15,7 @@
 // (every lane of a warp shares its k group).  That is 64 FFMA per 2 weight loads plus
 // (8 + S - 1)/4 input loads: the FP32 pipe, not shared memory, is the limit.
 // Handles any stride / padding / dilation / groups and NCHW or NHWC, fp32 or bf16.
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include "internal.h"
 #include "stage.cuh"
@@ -166,7 +167,10 @@ static cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     int FWp = (FW + 3 + 3) / 4 * 4;
     if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
     const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
-    const int budget = 48 * 1024;
+    static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (AI3_DIRECT_KB: A/B)
+        const char* e = getenv("AI3_DIRECT_KB");
+        return (e && atoi(e) >= 8 && atoi(e) <= 100) ? atoi(e) * 1024 : 48 * 1024;
+    }();
     int CB = budget / per_c;
     if (CB < 1) CB = 1;
     if (CB > a.Cg) CB = a.Cg;
