@@ -727,6 +727,7 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     const uint32_t stg_u32 = smem_u32(my_stg);
     const bool has_bias = a.bias != nullptr;
+    const bool stg_direct = a.store_mode == 3;
     // per-lane swizzled 16-byte slot offsets inside a staging buffer
     uint32_t qoff[BOX64 ? 8 : 4];
 #pragma unroll
@@ -827,6 +828,36 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 }
                 const bool last = col0 + 32 >= a.Ncols;
                 if (BOX64 && half == 0 && !last) continue;
+                if (stg_direct) {
+                    // store_mode 3: the warp re-reads its staged rows in 16-byte chunks and writes them
+                    // with coalesced st.global (4 or 8 consecutive output rows per instruction)
+                    __syncwarp();
+                    constexpr int CPR = ROWB / 16;  // 16-byte chunks per staged row
+                    const uint8_t* src = my_stg + slot * 32 * ROWB;
+                    const int cx = col0 - 32 * half;
+                    const int ncols_row = BOX64 ? 64 : 32;
+#pragma unroll
+                    for (int itc = 0; itc < CPR; ++itc) {
+                        const int idx = itc * 32 + lane, r = idx / CPR, q = idx % CPR;
+                        const int pq = BOX64 ? (q ^ (r & 7)) : (q ^ ((r >> 1) & 3));
+                        const uint4 v = *reinterpret_cast<const uint4*>(src + r * ROWB + (pq << 4));
+                        int64_t pixel;
+                        bool ok;
+                        if (HALO) {
+                            const int pp = row0 + r / a.TQ, qq = qc + r % a.TQ;
+                            ok = pp < a.P && qq < a.Q;
+                            pixel = ((int64_t)img * a.P + pp) * a.Q + qq;
+                        } else {
+                            const int m = row0 + r;
+                            ok = m < a.M;
+                            pixel = m;
+                        }
+                        if (ok && cx + q * 8 < a.Ncols && cx + q * 8 < cx + ncols_row)
+                            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + pixel * a.Ncols + cx + q * 8) = v;
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -957,7 +988,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = threadIdx.x - 64; i < a.Ncols; i += 32 * NUM_EPI_WARPS) sbias[i] = a.bias[i];
             named_bar_sync(1, 32 * NUM_EPI_WARPS);
         }
-        const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.store_mode == 1 && a.stg_row != 0 &&
+        const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && (a.store_mode == 1 || a.store_mode == 3) &&
+                          a.stg_row != 0 &&
                           (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
         if (a.n2 == 2 && !fast) __trap();  // N sub-tiles are configured for the fast epilogue only
@@ -1288,7 +1320,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     a.cg = pick_cg(a.M);
     {
         const char* e = getenv("AI3_TC_STORE");
-        a.store_mode = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+        a.store_mode = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;
         if (a.store_mode == 0 && !a.bias_smem) a.stg_row = 0;
     }
     {
@@ -1303,7 +1335,8 @@ void tc_configure(TcPlan& p, int num_sms) {
         const char* e = getenv("AI3_TC_DEBUG");
         a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
     }
-    if (a.n2 == 2 && (a.store_mode != 1 || !a.epi_fast || a.dbg || a.trace)) a.n2 = 1;  // fast epilogue only
+    if (a.n2 == 2 && ((a.store_mode != 1 && a.store_mode != 3) || !a.epi_fast || a.dbg || a.trace))
+        a.n2 = 1;  // fast epilogue only
     {
         const char* e = getenv("AI3_PF");  // L2 prefetch distance in scheduler steps (TILED2D)
         a.pf_tiles = (e && e[0] >= '0' && e[0] <= '9') ? atoi(e) : 0;

@@ -3,7 +3,8 @@ A/B switches (read when a plan is laid out):
 
 * flat mode (1x1 / stride 1 / no padding: A is the NHWC input itself, tiled TMA boxes);
 * AI3_FLAT1X1=0 (the same convs through the TMA im2col traversal);
-* AI3_HALO1X1=1 (1x1 convs with K <= 128 through the halo modes, the pre-round-1-end routing).
+* AI3_HALO1X1=1 (1x1 convs with K <= 128 through the halo modes, the pre-round-1-end routing);
+* AI3_TC_STORE=3 (fast epilogue writing its staged rows with coalesced st.global instead of TMA stores).
 """
 import numpy as np
 import pytest
@@ -35,7 +36,8 @@ def _run(shape, x, w, b, dtype, math, layout):
     return y.float().contiguous().cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("env", [None, ("AI3_FLAT1X1", "0"), ("AI3_HALO1X1", "1")], ids=["flat", "im2col", "halo"])
+@pytest.mark.parametrize("env", [None, ("AI3_FLAT1X1", "0"), ("AI3_HALO1X1", "1"), ("AI3_TC_STORE", "3")],
+                         ids=["flat", "im2col", "halo", "stg"])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: s.name)
 @pytest.mark.parametrize("dtype,math", MODES)
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])

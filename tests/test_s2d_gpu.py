@@ -78,7 +78,7 @@ def test_s2d_integer_stem_bit_exact(dtype, math):
     np.testing.assert_array_equal(y, r)
 
 
-@pytest.mark.parametrize("env", [("AI3_HALO32_SW", "1"), ("AI3_S2D_SPLIT", "0"), ("AI3_S2D_C64", "0")],
+@pytest.mark.parametrize("env", [("AI3_HALO32_SW", "1"), ("AI3_S2D_SPLIT", "0"), ("AI3_S2D_C64", "0"), ("AI3_TC_STORE", "3")],
                          ids=lambda e: e[0])
 @pytest.mark.parametrize("case", [CASES[0], CASES[1], CASES[-3]], ids=lambda c: c[0])
 def test_s2d_alternative_layouts(case, env, monkeypatch):
