@@ -16,7 +16,9 @@
  * (PAPER.md:104, :142, :170):
  *   AI3_ALGO_DIRECT         -- direct convolution, no data transform (§II.B(d))
  *   AI3_ALGO_GEMM           -- explicit IM2COL matrix + GEMM (§II.B(a), :194 §V.B(c))
- *   AI3_ALGO_IMPLICIT_GEMM  -- GEMM without forming the matrix, zero extra memory (§V.B(b))
+ *   AI3_ALGO_IMPLICIT_GEMM  -- GEMM without forming the im2col matrix (§V.B(b)); workspace only
+ *                              for an input layout / precision pass (NCHW, padded channels, fp32 operands)
+ *                              or, for strided few-channel convs, their space-to-depth image (R24)
  *   AI3_ALGO_WINOGRAD       -- Winograd minimal filtering F(2x2,3x3) (§V.B(d))
  *   AI3_ALGO_IMPLICIT_PRECOMP_GEMM -- implicit GEMM over a precomputed index table
  *   AI3_ALGO_SMM            -- scalar matrix multiplication: shifted planes x scalar weights
