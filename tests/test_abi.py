@@ -122,6 +122,28 @@ def test_guess_strided_rgb_stems_use_s2d_implicit_gemm(dtype):
     assert ai3.guess((256, 3, 224, 224), 64, 1, 2, 0, 1, 1, dtype=dtype) == "gemm"
 
 
+def test_guess_routes_narrow_channel_layers():
+    """bf16 stride-1 layers with 9..16 channels take the 32-byte-pixel halo (implicit_gemm); the
+    same layer in fp32 (64-byte pixels would need C >= 8 for a full row) stays on gemm."""
+    assert ai3.guess((64, 12, 112, 112), 64, 3, 1, 1, 1, 1, dtype=torch.bfloat16) == "implicit_gemm"
+    assert ai3.guess((64, 16, 112, 112), 64, 5, 1, 2, 1, 1, dtype=torch.bfloat16) == "implicit_gemm"
+    assert ai3.guess((64, 3, 112, 112), 64, 3, 1, 1, 1, 1, dtype=torch.float32) == "gemm"
+
+
+def test_s2d_workspace_holds_the_s2d_image():
+    """R24: the implicit_gemm workspace of the ResNet stem (NHWC bf16 input) is the s2d image,
+    N x (P+T-1) x (Q+T-1) x 16 channels of bf16 (P = Q = 112, T = 4) plus the prepared weights."""
+    lib = _lib.load()
+    prm = _lib.params(64, (7, 7), (2, 2), (3, 3), (1, 1), 1, False)
+    out = ctypes.c_size_t()
+    st = lib.ai3_conv2d_workspace_size(ctypes.byref(prm), _lib.shape4((8, 3, 224, 224)), _lib.BF16, _lib.MATH_STRICT,
+                                       ai3.algo_id("implicit_gemm"), _lib.NHWC, _lib.NHWC, ctypes.byref(out))
+    assert st == 0, _lib.last_error()
+    image = 8 * 115 * 115 * 16 * 2
+    weights = 64 * 16 * 16 * 2
+    assert image + weights <= out.value <= image + weights + 4096
+
+
 def test_workspace_sizes():
     lib = _lib.load()
 
