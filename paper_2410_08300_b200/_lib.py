@@ -69,12 +69,21 @@ CUSTOM_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(Tensor4d), ctypes.POIN
 _lib = None
 
 
+def select_library(path: str) -> None:
+    """Load `path` instead of the in-tree libai3.so (the developer build libai3_dev.so, or the
+    deliberately faulty libai3_mutant.so of the mutation test).  Must precede the first load;
+    no environment variable can redirect the product's library."""
+    global LIB_PATH
+    if _lib is not None and os.path.abspath(path) != os.path.abspath(LIB_PATH):
+        raise RuntimeError(f"libai3 already loaded from {LIB_PATH}")
+    LIB_PATH = path
+
+
 def load():
     """Load libai3.so (building nothing).  Raises Ai3LibraryMissing if absent."""
     global _lib, LIB_PATH
     if _lib is not None:
         return _lib
-    LIB_PATH = os.environ.get("AI3_LIB", LIB_PATH)  # developer A/B builds; default: in-tree libai3.so
     if not os.path.exists(LIB_PATH):
         raise Ai3LibraryMissing(f"{LIB_PATH} not found: build it with `python -m paper_2410_08300_b200.build` "
                                 "(there is no CPU fallback)")

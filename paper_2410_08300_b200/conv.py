@@ -123,6 +123,15 @@ class _Workspace(threading.local):
 _WS = _Workspace()
 
 
+def _same_dtype(dt: torch.dtype, weight: torch.Tensor, bias: torch.Tensor | None):
+    """Weights (and bias) must already have the activation dtype, as F.conv2d requires; the
+    library converts nothing on the caller's behalf."""
+    if weight.dtype != dt or (bias is not None and bias.dtype != dt):
+        raise TypeError(f"input dtype {dt} differs from weight {weight.dtype}"
+                        + ("" if bias is None else f" / bias {bias.dtype}") + " (torch.nn.functional.conv2d "
+                        "raises on mixed dtypes too)")
+
+
 def _require_cuda(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -188,11 +197,10 @@ def conv2d(input: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None 
         raise ValueError("input and weight must be 4-D (NCHW / KCRS)")
     if isinstance(padding, str):
         raise UnsupportedConfiguration("string padding is not supported; pass integers")
+    _same_dtype(input.dtype, weight, bias)
     weight = weight.contiguous()
     if bias is not None:
         bias = bias.contiguous()
-        if bias.dtype != input.dtype:
-            bias = bias.to(input.dtype)
     in_layout = layout_of(input)
     s, p, d = _pair(stride), _pair(padding), _pair(dilation)
     oshape = output_shape(input.shape, weight.shape[0], weight.shape[2:], s, p, d, groups)
@@ -238,9 +246,10 @@ def autotune(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = 
     lib = _lib.load()
     if not (x.is_contiguous() or x.is_contiguous(memory_format=torch.channels_last)):
         x = x.contiguous()
-    weight = weight.detach().to(x.dtype).contiguous()
+    _same_dtype(x.dtype, weight, bias)
+    weight = weight.detach().contiguous()
     if bias is not None:
-        bias = bias.detach().to(x.dtype).contiguous()
+        bias = bias.detach().contiguous()
     in_layout = layout_of(x)
     out_layout = in_layout if out_layout is None else out_layout
     s, p, d = _pair(stride), _pair(padding), _pair(dilation)
@@ -299,9 +308,10 @@ class ConvPlan:
         lib = _lib.load()
         self.device = weight.device
         self.dtype = dtype or weight.dtype
-        weight = weight.detach().to(self.dtype).contiguous()
+        _same_dtype(self.dtype, weight, bias)
+        weight = weight.detach().contiguous()
         if bias is not None:
-            bias = bias.detach().to(self.dtype).contiguous()
+            bias = bias.detach().contiguous()
         self.in_shape = tuple(int(v) for v in in_shape)
         self.stride, self.padding, self.dilation, self.groups = _pair(stride), _pair(padding), _pair(dilation), groups
         self.math = math
@@ -337,9 +347,13 @@ class ConvPlan:
         fmt = torch.channels_last if self.in_layout == _lib.NHWC else torch.contiguous_format
         if not x.is_contiguous(memory_format=fmt):
             raise ValueError("input memory format differs from the plan's")
+        ofmt = torch.channels_last if self.out_layout == _lib.NHWC else torch.contiguous_format
         if out is None:
-            fmt = torch.channels_last if self.out_layout == _lib.NHWC else torch.contiguous_format
-            out = torch.empty(self.out_shape, dtype=self.dtype, device=self.device, memory_format=fmt)
+            out = torch.empty(self.out_shape, dtype=self.dtype, device=self.device, memory_format=ofmt)
+        elif (tuple(out.shape) != tuple(self.out_shape) or out.dtype != self.dtype or out.device != self.device
+              or not out.is_contiguous(memory_format=ofmt)):
+            raise ValueError(f"out must be a {self.out_shape} {self.dtype} tensor on {self.device} in the plan's "
+                             f"output memory format, got {tuple(out.shape)} {out.dtype} on {out.device}")
         ws = _WS.get(self.device, self.workspace_size)
         _check(_lib.load().ai3_conv2d_plan_execute(self._h, x.data_ptr(), out.data_ptr(),
                                                    None if ws is None else ws.data_ptr(),

@@ -176,8 +176,7 @@ ai3_status check_supported(const ConvProblem& c, ai3_algo algo) {
 // channels cannot fill a 32-byte K-block row (RGB stems: ResNet 7x7 s2, AlexNet 11x11 s4) runs as
 // the stride-1 conv of ceil(R/sh) x ceil(S/sw) taps over the s2d image of sh*sw*C channels.
 bool s2d_eligible(const ConvProblem& c) {
-    const char* e = getenv("AI3_S2D");
-    if (e && e[0] == '0') return false;
+    if (!knob("AI3_S2D", 1)) return false;
     const int64_t elem = c.dtype == AI3_BF16 ? 2 : 4;
     return c.G == 1 && c.dh == 1 && c.dw == 1 && (c.sh > 1 || c.sw > 1) && c.C * elem < 32 && c.R >= c.sh &&
            c.S >= c.sw && c.C * c.sh * c.sw <= 64 && c.H * c.W * c.C < INT32_MAX;  // prep: 32-bit in-image offsets
@@ -210,8 +209,7 @@ ai3_algo guess_rule(const ConvProblem& c) {
         // all R*S taps from one smem halo per tile with no im2col round trip
         const bool narrow_halo = c.dtype == AI3_BF16 && c.C <= 16 && c.sh == 1 && c.sw == 1 && c.dh == 1 &&
                                  c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 && c.N <= 65535;
-        const char* e = getenv("AI3_HALO");
-        if (narrow_halo && !(e && e[0] == '0')) return AI3_ALGO_IMPLICIT_GEMM;
+        if (narrow_halo && knob("AI3_HALO", 1)) return AI3_ALGO_IMPLICIT_GEMM;
         // ...or the strided conv has a space-to-depth view with full rows
         if (s2d_eligible(c) && check_supported(c, AI3_ALGO_IMPLICIT_GEMM) == AI3_OK) return AI3_ALGO_IMPLICIT_GEMM;
         g_err.clear();
@@ -239,6 +237,16 @@ ai3_status resolve_algo(const ConvProblem& c, ai3_algo algo, ai3_algo* out) {
 }  // namespace
 
 ai3_status ai3::api_fail(ai3_status st, const char* msg) { return fail(st, "%s", msg); }
+
+int ai3::knob(const char* name, int dflt) {
+#ifdef AI3_DEV_KNOBS
+    const char* e = getenv(name);
+    if (e && e[0]) return atoi(e);
+#else
+    (void)name;
+#endif
+    return dflt;
+}
 
 // ---------------------------------------------------------------- the plan
 struct ai3_plan {
@@ -320,22 +328,17 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     }
     pl.Cpad = padded_channels(c.C, pl.elem);
     // s2d views with 33..63 channels (AlexNet conv1: 48): pad to one 64-channel halo chunk
-    // rather than 32-byte im2col rows (AI3_S2D_C64=0 keeps the narrow rows, for A/B)
-    if (pl.s2d && pl.cm == CM_BF16 && pl.Cpad > 32 && pl.Cpad < 64 && c.K <= 128) {
-        const char* e6 = getenv("AI3_S2D_C64");
-        if (!(e6 && e6[0] == '0')) pl.Cpad = 64;
-    }
+    // rather than 32-byte im2col rows
+    if (pl.s2d && pl.cm == CM_BF16 && pl.Cpad > 32 && pl.Cpad < 64 && c.K <= 128) pl.Cpad = 64;
     pl.Kp = algo == AI3_ALGO_KN2ROW ? pl.Cpad : round_up(c.R * c.S * c.C, 16 / pl.elem);
     // halo modes (implicit GEMM, bf16, stride 1, undilated, K <= 128): 64 channels per pixel
     // (128-byte swizzled rows), or <= 8 channels padded to 8 (16-byte rows, RGB first layers)
     pl.halo_pb = 0;
     {
-        const char* e = getenv("AI3_HALO");
-        const bool allow = !(e && e[0] == '0');
+        const bool allow = knob("AI3_HALO", 1) != 0;
         // 1x1 convs take the flat mode below (a halo of a 1x1 filter is just the tile, and the
-        // 16x8-pixel halo tiles pad 28x28 / 14x14 maps); AI3_HALO1X1=1 keeps them in halo mode (A/B)
-        const char* e1 = getenv("AI3_HALO1X1");
-        const bool not1x1 = !(c.R == 1 && c.S == 1) || (e1 && e1[0] == '1');
+        // 16x8-pixel halo tiles pad 28x28 / 14x14 maps)
+        const bool not1x1 = !(c.R == 1 && c.S == 1);
         const bool shape_ok = not1x1 && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
                               c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
                               c.N <= 65535;
@@ -345,9 +348,8 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         if (allow && shape_ok && c.C > 8 && c.C <= 16) { pl.halo_pb = 32; pl.Cpad = 16; }
         // chunked halo: 64-channel chunks of wider inputs, weights streamed per (chunk, tap);
         // K <= 128 (measured: VGG conv2_2 238 -> 220 us; at K = 256 the im2col mode was as
-        // fast or faster).  AI3_HALO_CHUNKED=0 turns it off (A/B)
-        const char* ec = getenv("AI3_HALO_CHUNKED");
-        const bool allow_c = allow && !(ec && ec[0] == '0');
+        // fast or faster)
+        const bool allow_c = allow && knob("AI3_HALO_CHUNKED", 1) != 0;
         const bool shape_c = not1x1 && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
                              c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
                              c.N <= 65535 && pl.Cpad % 64 == 0 && pl.Cpad >= 128;
@@ -413,23 +415,13 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.TP = 16; a.TQ = 8; a.RS = 16; a.HR = a.TP + (int)c.R - 1;
         a.halo_pb = pl.halo_pb;
         a.halo_chunks = pl.halo_pb == 128 ? (int)(pl.Cpad / 64) : 1;
-        if (pl.halo_pb == 32) {
-            // s2d views: the prep writes plane-split rows, loaded as one 256-byte-row box per halo
-            // (AI3_S2D_SPLIT=0: NHWC).  NHWC sources: two 8-channel planes (16-byte box rows), or
-            // one SWIZZLE_32B box of whole pixels (AI3_HALO32_SW=1).  Same-box, ResNet stem:
-            // 220 / 231 / 224 us
-            const char* e = getenv("AI3_HALO32_SW");
-            const char* es = getenv("AI3_S2D_SPLIT");
-            a.halo32 = pl.s2d && !(es && es[0] == '0') ? 2 : (e && e[0] == '1' ? 1 : 0);
-        }
+        // 32-byte pixels: s2d views are written by the prep as plane-split rows, loaded as one
+        // 256-byte-row box per halo; NHWC sources load two 8-channel planes (16-byte box rows)
+        if (pl.halo_pb == 32) a.halo32 = pl.s2d ? 2 : 0;
         a.taps_pad = (int)pl.taps_pad;
         a.batch_images = (int)c.N;
-        {
-            // the tensor core applies the 128B swizzle on absolute smem address bits, so a view
-            // starting mid-atom needs no base offset (measured: base offset on -> wrong results)
-            const char* e = getenv("AI3_HALO_BO");
-            a.halo_bo = (e && e[0] == '1') ? 1 : 0;
-        }
+        // (the tensor core applies the 128B swizzle on absolute smem address bits, so a tap
+        // view starting mid-atom needs no descriptor base offset)
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
         a.a_mode = TC_A_GATHER;
@@ -440,7 +432,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.gather_rows = (int)pl.idx_rows;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_GEMM && c.R == 1 && c.S == 1 && c.sh == 1 && c.sw == 1 && c.ph == 0 &&
-               c.pw == 0 && !(getenv("AI3_FLAT1X1") && getenv("AI3_FLAT1X1")[0] == '0')) {
+               c.pw == 0) {
         // 1x1, stride 1, no padding: the A operand is the NHWC input [N*H*W][Cpad] itself, loaded
         // with plain tiled TMA boxes (no im2col traversal)
         pl.flat = 1;
@@ -508,9 +500,8 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     tc_configure(pl.tc, device_num_sms());
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
     {
-        const char* e = getenv("AI3_BOX64");
-        const bool allow = !(e && e[0] == '0');
-        if (allow && a.store_mode == 1 && a.stg_row == 64 && a.out_bf16 && a.block_n % 64 == 0 && a.batch == 1) {
+        const bool allow = knob("AI3_BOX64", 1) != 0;
+        if (allow && a.stg_row == 64 && a.out_bf16 && a.block_n % 64 == 0 && a.batch == 1) {
             a.box64 = 1;
             a.stg_row = 128;
             tc_configure(pl.tc, device_num_sms());  // re-derive stages / staging with 4 KB buffers
@@ -579,17 +570,16 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
             const uint32_t box[4] = {(uint32_t)(a.halo_chunks > 1 ? 64 : pl.Cpad), (uint32_t)a.RS, (uint32_t)a.HR, 1};
             oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
         } else if (a.halo_pb == 32) {
-            // 32-byte pixels: two loads of 8-channel planes (16-byte box rows), or one
-            // SWIZZLE_32B load of whole pixels (AI3_HALO32_SW=1)
+            // 32-byte pixels: two loads of 8-channel planes (16-byte box rows), or one load
+            // of plane-split rows (s2d prep)
             if (a.halo32 == 2) {
                 const uint64_t d4[4] = {(uint64_t)c.W * 8, 2, (uint64_t)c.H, (uint64_t)c.N};
                 const uint64_t s4[3] = {c.W * 8 * e, c.W * 16 * e, c.H * c.W * 16 * e};
                 const uint32_t box[4] = {(uint32_t)a.RS * 8, 2, (uint32_t)a.HR, 1};
                 oka = encode_tiled(&pl.ta0, dt, 4, src, d4, s4, box, CU_TENSOR_MAP_SWIZZLE_NONE);
             } else {
-                const uint32_t box[4] = {a.halo32 == 1 ? 16u : 8u, (uint32_t)a.RS, (uint32_t)a.HR, 1};
-                oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box,
-                                   a.halo32 == 1 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+                const uint32_t box[4] = {8u, (uint32_t)a.RS, (uint32_t)a.HR, 1};
+                oka = encode_tiled(&pl.ta0, dt, 4, src, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
             }
         } else {
             // 16-byte pixels: view the rows as (W*Cpad, H, N) so that each halo row is one
@@ -786,7 +776,13 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.bias = nullptr;
         tp.args.relu = 0;
     }
-    if (tp.args.stg_row && !aligned(tp.args.out, 16)) tp.args.stg_row = 0;  // TMA needs a 16-byte base
+    if (tp.args.stg_row && !aligned(tp.args.out, 16)) {  // TMA stores need a 16-byte base
+        if (tp.args.n2 == 2)  // two N sub-tiles per unit run only with the TMA-store epilogue
+            return fail(AI3_ERR_INVALID_ARGUMENT, "y must be 16-byte aligned for this plan (%s, %lld output channels)",
+                        ai3_algo_name(pl.algo), (long long)c.K);
+        tp.args.stg_row = 0;
+        tp.args.box64 = 0;
+    }
     if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
     e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
@@ -921,6 +917,7 @@ ai3_status ai3_conv2d_plan_create(const ai3_conv2d_params* params, const int64_t
                                   ai3_math math, ai3_algo algo, int32_t in_layout, int32_t out_layout, const void* w,
                                   const void* bias, void* weight_buf, size_t weight_bytes, void* stream,
                                   ai3_plan** out) {
+    StreamDeviceGuard device_guard(stream);
     if (!out) return fail(AI3_ERR_INVALID_ARGUMENT, "null out");
     *out = nullptr;
     ConvProblem c{};
@@ -959,12 +956,14 @@ int ai3_conv2d_plan_num_launches(const ai3_plan* plan) { return plan ? plan->lau
 
 ai3_status ai3_conv2d_plan_execute(ai3_plan* plan, const void* x, void* y, void* workspace, size_t workspace_bytes,
                                    void* stream) {
+    StreamDeviceGuard device_guard(stream);
     if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
     return execute(*plan, x, y, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void* y_host, void* x_dev, void* y_dev,
                                         void* workspace, size_t workspace_bytes, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
     if (!x_host || !y_host || !x_dev || !y_dev) return fail(AI3_ERR_INVALID_ARGUMENT, "null host or staging buffer");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -980,6 +979,7 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
 ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, const void* const* x_hosts,
                                          void* const* y_hosts, void* const* x_devs, void* const* y_devs,
                                          void* workspace, size_t workspace_bytes, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     if (n < 0 || (n > 0 && (!plans || !x_hosts || !y_hosts || !x_devs || !y_devs)))
         return fail(AI3_ERR_INVALID_ARGUMENT, "null plan / buffer array");
     for (int32_t i = 0; i < n; ++i)
@@ -1074,6 +1074,7 @@ ai3_status ai3_conv2d_plan_set_relu(ai3_plan* plan, int32_t relu) {
 ai3_status ai3_conv2d(const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias, const int32_t stride[2],
                       const int32_t padding[2], const int32_t dilation[2], int32_t groups, ai3_algo algo,
                       ai3_math math, ai3_tensor4d* y, void* workspace, size_t workspace_bytes, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     ai3_status s;
     if ((s = check_tensor(x, "x")) != AI3_OK || (s = check_tensor(w, "w")) != AI3_OK ||
         (s = check_tensor(y, "y")) != AI3_OK)

@@ -94,6 +94,7 @@ ai3_status ai3_conv2d_autotune(const ai3_conv2d_params* params, const int64_t in
                                ai3_math math, int32_t in_layout, int32_t out_layout, const void* x, const void* w,
                                const void* bias, void* y, void* scratch, size_t scratch_bytes, int32_t reps,
                                void* stream, ai3_algo* best, float* ms_per_algo) {
+    StreamDeviceGuard device_guard(stream);
     if (!params || !in_shape || !x || !w || !y || !best)
         return api_fail(AI3_ERR_INVALID_ARGUMENT, "autotune: null argument");
     if (reps < 1) reps = 1;

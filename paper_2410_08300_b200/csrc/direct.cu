@@ -167,9 +167,9 @@ static cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     int FWp = (FW + 3 + 3) / 4 * 4;
     if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
     const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
-    static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (AI3_DIRECT_KB: A/B)
-        const char* e = getenv("AI3_DIRECT_KB");
-        return (e && atoi(e) >= 8 && atoi(e) <= 100) ? atoi(e) * 1024 : 48 * 1024;
+    static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (dev knob AI3_DIRECT_KB)
+        const int kb = knob("AI3_DIRECT_KB", 48);
+        return (kb >= 8 && kb <= 100 ? kb : 48) * 1024;
     }();
     int CB = budget / per_c;
     if (CB < 1) CB = 1;

@@ -12,6 +12,34 @@ namespace ai3 {
 // Set the thread-local ai3_last_error message and return `st` (api.cu).
 ai3_status api_fail(ai3_status st, const char* msg);
 
+// Developer knobs for A/B experiments (tile sizes, ring depths, routing switches between
+// equally exact modes).  The product library reads NO environment variable: knob()
+// returns `dflt` unless libai3 was compiled with -DAI3_DEV_KNOBS (python -m
+// paper_2410_08300_b200.build --dev), in which case it returns atoi(getenv(name)) when set.
+int knob(const char* name, int dflt);
+
+// Make the stream's device current for the lifetime of the guard (and restore the previous
+// device after): every C-ABI entry point that launches work takes the caller's stream, which
+// may belong to a device other than the calling thread's current one.  The legacy default
+// stream (null) is the current device's.
+struct StreamDeviceGuard {
+    int prev = -1;
+    explicit StreamDeviceGuard(void* stream) {
+        if (!stream) return;
+        int sd = -1, cur = -1;
+        if (cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), &sd) != cudaSuccess) {
+            (void)cudaGetLastError();  // not a stream handle cudart knows: leave the device alone
+            return;
+        }
+        if (cudaGetDevice(&cur) == cudaSuccess && sd != cur && cudaSetDevice(sd) == cudaSuccess) prev = cur;
+    }
+    ~StreamDeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    StreamDeviceGuard(const StreamDeviceGuard&) = delete;
+    StreamDeviceGuard& operator=(const StreamDeviceGuard&) = delete;
+};
+
 struct ConvProblem;
 // The algorithm ai3_conv2d_autotune measured fastest for this problem, if any (autotune.cu).
 bool autotune_lookup(const ConvProblem& c, ai3_algo* out);
@@ -127,8 +155,7 @@ struct TcArgs {
     int promote_kb; // 3xTF32: K-blocks per TMEM accumulation chunk summed in fp32 registers (0 = whole K)
     int stages;
     int epi_fast;   // 1: use the compile-time-specialised bf16 TMA-store epilogue when it applies
-    int trace;      // 1: accumulate pipeline-wait cycles in g_tc_trace (AI3_TC_TRACE=1)
-    int dbg;        // 0 normal; 1 = no MMA (TMA pipeline only); 2 = no TMA (MMA on stale smem); 3 = no epilogue stores -- timing probes
+    int trace;      // 1: accumulate pipeline-wait cycles in g_tc_trace (dev builds only: knob AI3_TC_TRACE)
     int n_acc;      // TMEM accumulator buffers (2..8)
     int n_stg;      // epilogue smem staging buffers per warp (2, 4 or 8)
     int cg;         // CTAs per MMA group: 1 or 2 (cta_group::2 pair, 256-row tiles)
@@ -138,10 +165,10 @@ struct TcArgs {
     // halo mode (a_mode == TC_A_HALO, stride 1, one 64-channel chunk): each CTA computes a
     // TP x TQ output-pixel tile from one (TP+R-1) x RS-slot input halo held in smem; the
     // R*S weight taps stay resident in smem for the whole kernel
-    int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, halo_bo, batch_images;
+    int P, R, TP, TQ, RS, HR, tiles_p, tiles_q, halo_bytes, bres_bytes, batch_images;
     int halo_pb;    // bytes per halo pixel: 128 (64 channels, SWIZZLE_128B), 32 (16 channels: two 8-channel planes) or 16 (<= 8 channels), no swizzle below 128
-    int halo32;     // halo_pb == 32 source: 0 = NHWC pixels, two 8-channel plane loads; 1 = NHWC pixels, one
-                    // SWIZZLE_32B load; 2 = plane-split rows [n][h][2][w][8] (s2d prep), one 256-byte-row load
+    int halo32;     // halo_pb == 32 source: 0 = NHWC pixels, two 8-channel plane loads;
+                    // 2 = plane-split rows [n][h][2][w][8] (s2d prep), one 256-byte-row load
     int taps_pad;   // weight taps held in smem (R*S, rounded up to even for 16-byte pixels)
     // chunked halo (halo_chunks > 1: Cpad = 64 * halo_chunks channels, K <= 256): per tile and
     // 64-channel chunk one halo from a ring of hslots; the weights stream per (chunk, tap)
@@ -151,10 +178,9 @@ struct TcArgs {
     int out_nchw;   // 1: out[b][n][k][pq] with n = m / PQ (PQ given); 0: out[b][m][k]
     int out_bf16;
     int epi_PQ;
-    int stg_row;    // TMA-store epilogue: bytes per staged row (32 * out elem); 0 = direct stores
+    int stg_row;    // TMA-store epilogue: bytes per staged row (32 * out elem); 0 = direct per-row stores
     int bias_smem;  // 1: the epilogue stages the fp32 bias in shared memory
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
-    int store_mode; // 0 direct per-row stores; 1 TMA bulk-tensor store; 2 smem-transposed coalesced stores
     int relu;       // 1: fused ReLU after the bias (model path)
     int pf_tiles;   // TILED2D: prefetch the A panel of the tile this many scheduler steps ahead into L2 (0 = off)
     int n2;         // N sub-tiles per unit (1, or 2: one A stage feeds two block_n-column MMAs --

@@ -247,6 +247,7 @@ using namespace ai3;
 extern "C" {
 
 ai3_status ai3_relu(const void* x, void* y, int64_t numel, int32_t dtype, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     if (!x || !y) return api_fail(AI3_ERR_INVALID_ARGUMENT, "relu: null x / y");
     if (numel < 0) return api_fail(AI3_ERR_INVALID_ARGUMENT, "relu: numel < 0");
     if (dtype != AI3_F32 && dtype != AI3_BF16) return api_fail(AI3_ERR_INVALID_ARGUMENT, "relu: unknown dtype");
@@ -333,14 +334,17 @@ static ai3_status pool_common(const ai3_tensor4d* x, const ai3_pool2d_params* p,
 }
 
 ai3_status ai3_maxpool2d(const ai3_tensor4d* x, const ai3_pool2d_params* p, ai3_tensor4d* y, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     return pool_common(x, p, y, true, stream);
 }
 
 ai3_status ai3_avgpool2d(const ai3_tensor4d* x, const ai3_pool2d_params* p, ai3_tensor4d* y, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     return pool_common(x, p, y, false, stream);
 }
 
 ai3_status ai3_adaptive_avgpool2d(const ai3_tensor4d* x, ai3_tensor4d* y, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     ai3_status s;
     if ((s = check_act(x, "x")) != AI3_OK || (s = check_act(y, "y")) != AI3_OK) return s;
     if (x->dtype != y->dtype || x->layout != y->layout)
@@ -353,6 +357,7 @@ ai3_status ai3_adaptive_avgpool2d(const ai3_tensor4d* x, ai3_tensor4d* y, void* 
 }
 
 ai3_status ai3_layout_copy(const ai3_tensor4d* x, ai3_tensor4d* y, void* stream) {
+    StreamDeviceGuard device_guard(stream);
     ai3_status s;
     if ((s = check_act(x, "x")) != AI3_OK || (s = check_act(y, "y")) != AI3_OK) return s;
     if (x->dtype != y->dtype) return api_fail(AI3_ERR_INVALID_ARGUMENT, "layout_copy: dtypes differ");

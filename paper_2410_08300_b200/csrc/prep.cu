@@ -370,8 +370,14 @@ cudaError_t launch_gather_table(int* idx, int64_t M, int64_t rows, int64_t H, in
 }
 
 __global__ void bias_f32_kernel(const void* __restrict__ b, int bf16, int64_t K, float* __restrict__ dst) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+#ifdef AI3_MUTANT_DROP_BIAS
+        // deliberately faulty test build (libai3_mutant.so, tests/test_mutation_gpu.py): an
+        // off-by-one that loses the last output channel's bias -- parity must catch it
+        if (i == K - 1) { dst[i] = 0.f; continue; }
+#endif
         dst[i] = load_as_f32(b, i, bf16);
+    }
 }
 
 cudaError_t launch_bias_f32(const void* b, ai3_dtype dtype, int64_t K, float* dst, cudaStream_t st) {

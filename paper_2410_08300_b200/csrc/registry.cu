@@ -139,6 +139,7 @@ ai3_status ai3_conv2d_resolve(const char* name, ai3_algo* algo, char* custom_nam
 ai3_status ai3_conv2d_custom(const char* name, const ai3_tensor4d* x, const ai3_tensor4d* w, const void* bias,
                              const int32_t stride[2], const int32_t padding[2], const int32_t dilation[2],
                              int32_t groups, ai3_tensor4d* y, void* stream) {
+    ai3::StreamDeviceGuard device_guard(stream);
     if (!name) return ai3::api_fail(AI3_ERR_INVALID_ARGUMENT, "custom: null name");
     Entry e;
     bool found = false;

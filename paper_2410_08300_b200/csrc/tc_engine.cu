@@ -189,8 +189,6 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
                     tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
                     tma_load_2d_cg2(sB + b_bytes, &tb0, bar, kx, n0 + a.block_n);
                 }
-            } else if (a.dbg == 2) {  // timing probe: no loads, just hand the stage over
-                if (leader) mbar_arrive(&full[stage]);
             } else if (CG == 1) {
                 uint64_t* bar = &full[stage];
                 mbar_arrive_expect_tx(bar, stage_bytes);
@@ -330,7 +328,6 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
     const uint64_t alo_off = a_bytes >> 4, blo_off = b_bytes >> 4;
     const int tiles = a.m_tiles * a.n_tiles * a.batch;
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
-    const bool no_mma = a.dbg == 1;
     int stage = 0, acc = 0, kc = 0;
     uint32_t phase = 0, acc_phase = 0;
     uint32_t d_tmem = tmem_base;
@@ -346,7 +343,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
             tc_fence_after();
             const uint64_t soff = (uint64_t)((stage * stage_bytes) >> 4);
             const uint64_t ad = a_desc0 + soff, bd = b_desc0 + soff;
-            if (!no_mma && CMODE == CM_BF16 && a.n2 == 2) {  // same A, B sub-tile +b_bytes, D +block_n
+            if (CMODE == CM_BF16 && a.n2 == 2) {  // same A, B sub-tile +b_bytes, D +block_n
 #pragma unroll
                 for (int k = 0; k < KS; ++k) {
                     const uint32_t accum = (k > 0 || kc > 0) ? 1u : 0u;
@@ -359,7 +356,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
                         mma_bf16(d_tmem + a.block_n, adk, bdk + blo_off, idesc, accum);
                     }
                 }
-            } else if (!no_mma) {
+            } else {
 #pragma unroll
                 for (int k = 0; k < KS; ++k) {
                     const uint32_t accum = (k > 0 || kc > 0) ? 1u : 0u;
@@ -441,9 +438,7 @@ __device__ __forceinline__ void producer_halo(const TcArgs& a, const CUtensorMap
         halo_tile(a, tile, CG, rank, n, p0, q0);
         TRACE_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
         uint8_t* sA = smem + stage * sm.stage_bytes;
-        if (a.dbg == 2) {
-            if (rank == 0) mbar_arrive(&full[stage]);
-        } else if (CG == 1) {
+        if (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], sm.stage_bytes);
             if (a.halo_pb == 16)  // (W*8, H, N) view: one 256-byte TMA row per halo row
                 tma_load_3d(sA, &ta0, &full[stage], (q0 - a.pw) * 8, p0 - a.ph, n);
@@ -482,7 +477,6 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
     const uint32_t idesc = make_idesc(BM * CG, a.block_n, 1u);
     const uint32_t s0 = smem_u32(smem);
     const uint32_t sB = s0 + sm.bres_off;
-    const bool no_mma = a.dbg == 1;
     const bool narrow = a.halo_pb == 16;
     const bool planes2 = a.halo_pb == 32;
     const int RSl = a.RS;  // halo row stride in pixels
@@ -502,23 +496,20 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
         TRACE_WAIT(2, mbar_wait(&full[stage], phase));
         tc_fence_after();
         const uint32_t soff16 = (stage * sm.stage_bytes) >> 4;
-        if (!no_mma && planes2) {
+        if (planes2) {
             // 32-byte pixels as two 8-channel planes, no swizzle: one K=16 slice = one tap;
             // its second 8 channels sit one plane (LBO) further
             const uint32_t sbo_n = (uint32_t)RSl * 16u;
             const uint32_t plane = (uint32_t)(a.HR * RSl * 16);
             const uint32_t sA = s0 + stage * sm.stage_bytes;
             const int taps = a.R * a.S;
-            // descriptor of tap (r, s) = base + (r*row + s) * step (16-byte units), built per layout:
+            // descriptor of tap (r, s) = base + (r*row + s) (16-byte units), built per layout:
             //  0: two planes, pixels 16 B apart, plane 1 at LBO = plane, rows SBO = RS*16;
-            //  1: SWIZZLE_32B whole pixels, 32 B apart, rows SBO = RS*32;
             //  2: plane-split rows [HR][2][RS][8]: plane 1 at LBO = RS*16, rows SBO = 2*RS*16
             const int mode = a.halo32;
-            const uint64_t ad0 = mode == 1 ? make_sdesc_sw32(sA, sbo_n * 2u)
-                                 : mode == 2 ? make_sdesc_none(sA, sbo_n, sbo_n * 2u)
-                                             : make_sdesc_none(sA, plane, sbo_n);
+            const uint64_t ad0 = mode == 2 ? make_sdesc_none(sA, sbo_n, sbo_n * 2u) : make_sdesc_none(sA, plane, sbo_n);
             const uint32_t row16 = (uint32_t)RSl * (mode == 0 ? 1u : 2u);  // halo row, 16-byte units
-            const uint32_t px16 = mode == 1 ? 2u : 1u;                       // pixel step, 16-byte units
+            const uint32_t px16 = 1u;                                        // pixel step, 16-byte units
             int r = 0, s = 0;
             for (int t = 0; t < taps; ++t) {
                 const uint64_t ad = ad0 + (uint64_t)((uint32_t)r * row16 + (uint32_t)s * px16);
@@ -527,7 +518,7 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
                 else mma_bf16(d_tmem, ad, bd, idesc, t > 0);
                 if (++s == a.S) { s = 0; ++r; }
             }
-        } else if (!no_mma && narrow) {
+        } else if (narrow) {
             // 16-byte pixels, no swizzle: one K=16 slice = two filter taps; the second tap's
             // core matrices sit LBO = (its halo offset - the first's) bytes further
             const int taps = a.R * a.S;
@@ -562,7 +553,7 @@ __device__ __forceinline__ void mma_issuer_halo(const TcArgs& a, uint8_t* smem, 
                     if (c0 == a.S) { c0 = 0; ++r0; }
                 }
             }
-        } else if (!no_mma) {
+        } else {
             // 64-channel pixels, 128B swizzle: tap (r, s) view starts (r*RS + s) rows in; its
             // 8-row groups are RS rows apart; 4 K slices of 32 bytes per tap
             const uint64_t ad0 = a0_wide + soff16;
@@ -727,7 +718,6 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     const uint32_t stg_u32 = smem_u32(my_stg);
     const bool has_bias = a.bias != nullptr;
-    const bool stg_direct = a.store_mode == 3;
     // per-lane swizzled 16-byte slot offsets inside a staging buffer
     uint32_t qoff[BOX64 ? 8 : 4];
 #pragma unroll
@@ -828,36 +818,6 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 }
                 const bool last = col0 + 32 >= a.Ncols;
                 if (BOX64 && half == 0 && !last) continue;
-                if (stg_direct) {
-                    // store_mode 3: the warp re-reads its staged rows in 16-byte chunks and writes them
-                    // with coalesced st.global (4 or 8 consecutive output rows per instruction)
-                    __syncwarp();
-                    constexpr int CPR = ROWB / 16;  // 16-byte chunks per staged row
-                    const uint8_t* src = my_stg + slot * 32 * ROWB;
-                    const int cx = col0 - 32 * half;
-                    const int ncols_row = BOX64 ? 64 : 32;
-#pragma unroll
-                    for (int itc = 0; itc < CPR; ++itc) {
-                        const int idx = itc * 32 + lane, r = idx / CPR, q = idx % CPR;
-                        const int pq = BOX64 ? (q ^ (r & 7)) : (q ^ ((r >> 1) & 3));
-                        const uint4 v = *reinterpret_cast<const uint4*>(src + r * ROWB + (pq << 4));
-                        int64_t pixel;
-                        bool ok;
-                        if (HALO) {
-                            const int pp = row0 + r / a.TQ, qq = qc + r % a.TQ;
-                            ok = pp < a.P && qq < a.Q;
-                            pixel = ((int64_t)img * a.P + pp) * a.Q + qq;
-                        } else {
-                            const int m = row0 + r;
-                            ok = m < a.M;
-                            pixel = m;
-                        }
-                        if (ok && cx + q * 8 < a.Ncols && cx + q * 8 < cx + ncols_row)
-                            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + pixel * a.Ncols + cx + q * 8) = v;
-                    }
-                    __syncwarp();
-                    continue;
-                }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -988,11 +948,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = threadIdx.x - 64; i < a.Ncols; i += 32 * NUM_EPI_WARPS) sbias[i] = a.bias[i];
             named_bar_sync(1, 32 * NUM_EPI_WARPS);
         }
-        const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && (a.store_mode == 1 || a.store_mode == 3) &&
-                          a.stg_row != 0 &&
-                          (a.bias == nullptr || a.bias_smem) && a.dbg == 0 && !a.trace && a.batch == 1 &&
+        const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.stg_row != 0 &&
+                          (a.bias == nullptr || a.bias_smem) && !a.trace && a.batch == 1 &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
-        if (a.n2 == 2 && !fast) __trap();  // N sub-tiles are configured for the fast epilogue only
+        // invariant: N sub-tiles are configured for the fast epilogue only (tc_configure), and
+        // execute() rejects outputs that would turn the TMA stores off for such a plan
+        if (a.n2 == 2 && !fast) __trap();
         if (fast) {
             const uint32_t sb = smem_u32(sbias);
             if (a.a_mode == TC_A_HALO) {
@@ -1014,17 +975,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else mbar_arrive_relaxed(&tempty[which]);
             }
         };
-        // one 32-row x 32-column chunk of this warp: + bias, cast, store
         // one 32-row x 32-column chunk of this warp: + bias, cast, store.
-        //   store_mode 0: each lane stores its own row (direct STG);
-        //   store_mode 1: stage in smem (swizzled), one TMA bulk-tensor store per chunk;
-        //   store_mode 2: stage in smem, re-read transposed so that consecutive lanes write
-        //                 consecutive 16-byte pieces of the same row (full-sector STG).
+        //   stg_row == 0: each lane stores its own row (direct STG; NCHW outputs);
+        //   otherwise:    stage in smem (swizzled), one TMA bulk-tensor store per chunk.
         const uint32_t sbias_u32 = smem_u32(sbias);
         const uint32_t stg_u32 = smem_u32(my_stg);
         auto store_chunk = [&](float (&f)[32], int col0, int m_row0, int64_t base, int64_t cstride, bool row_ok,
                                int b, int q0c) {
-            if (a.dbg == 3) return;
             if (a.bias) {
                 if (a.bias_smem && col0 + 32 <= a.Ncols) {
 #pragma unroll
@@ -1042,7 +999,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];
             }
-            if (a.stg_row == 0 || a.store_mode == 0) {
+            if (a.stg_row == 0) {
                 if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
                 return;
             }
@@ -1051,7 +1008,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int half = a.box64 ? ((col0 >> 5) & 1) : 0;
             const int slot = nstore % a.n_stg;
             const uint32_t buf = stg_u32 + slot * 32 * a.stg_row;
-            if (a.store_mode == 1 && nstore >= a.n_stg && half == 0) {  // the store that used this slot must have read it
+            if (nstore >= a.n_stg && half == 0) {  // the store that used this slot must have read it
                 const unsigned long long tw0 = a.trace ? clock64() : 0ull;
                 if (lane == 0) {
                     if (a.n_stg == 8) bulk_wait_group_read<7>();
@@ -1085,7 +1042,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     sts128(buf + lane * 128 + ((q ^ (lane & 7)) << 4), *reinterpret_cast<const uint4*>(&v4));
                 }
             }
-            if (a.store_mode == 1) {
+            {
                 const bool last = col0 + 32 >= a.Ncols;
                 if (a.box64 && half == 0 && !last) return;  // wait for the second half of the row
                 fence_proxy_async_smem();
@@ -1097,24 +1054,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     else tma_store_2d(&tout, my_stg + slot * 32 * a.stg_row, cx, m_row0);
                     bulk_commit_group();
                 }
-            } else {
-                __syncwarp();
-                const int eo = a.out_bf16 ? 2 : 4;
-                const int per_row = a.stg_row >> 4;        // 16B pieces per row: 4 (bf16) or 8 (fp32)
-                const int rows_per_inst = 32 / per_row;    // 8 or 4
-                const int q = lane % per_row;
-                char* out = reinterpret_cast<char*>(a.out) + ((int64_t)b * a.out_bstride + col0) * eo;
-                const int valid16 = min(per_row, (a.Ncols - col0) * eo / 16);  // whole 16B pieces in range
-                const int64_t ldb = (int64_t)a.Ncols * eo;
-#pragma unroll 4
-                for (int i = 0; i < per_row; ++i) {
-                    const int r = i * rows_per_inst + lane / per_row;
-                    const int phys = a.out_bf16 ? (q ^ ((r >> 1) & 3)) : (q ^ (r & 7));
-                    const uint4 v = lds128(buf + r * a.stg_row + (phys << 4));
-                    const int mr = m_row0 + r;
-                    if (mr < a.M && q < valid16) *reinterpret_cast<uint4*>(out + (int64_t)mr * ldb + q * 16) = v;
-                }
-                __syncwarp();
             }
             ++nstore;
         };
@@ -1232,7 +1171,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         store_chunk(racc[c], n0 + c * 32, m_row0, base, cstride, row_ok, b, hq0);
             }
         }
-        if (lane == 0 && a.store_mode == 1) bulk_wait_group<0>();  // smem must outlive the last TMA stores
+        if (lane == 0 && a.stg_row != 0) bulk_wait_group<0>();  // smem must outlive the last TMA stores
         if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][6] += clock64() - t_epi0;
         __syncwarp();
     }
@@ -1280,21 +1219,14 @@ static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups,
 // CTA-group size: 2 (CTA pair, cta_group::2) unless the problem has a single 128-row
 // M tile.  AI3_TC_CG=1|2 overrides (A/B experiments).
 static int pick_cg(int M) {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = getenv("AI3_TC_CG");
-        env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-    }
-    if (env) return env;
+    const int forced = knob("AI3_TC_CG", 0);
+    if (forced == 1 || forced == 2) return forced;
     return M > BM ? 2 : 1;
 }
 
 void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
-    if (a.block_n == 0 && a.a_mode != TC_A_HALO) {
-        const char* e = getenv("AI3_BN");  // experiment override: force BLOCK_N
-        if (e && atoi(e) > 0) a.block_n = atoi(e);
-    }
+    if (a.block_n == 0 && a.a_mode != TC_A_HALO) a.block_n = knob("AI3_BN", 0);  // dev override: force BLOCK_N
     if (a.n2 != 2) a.n2 = 1;  // a re-configure (box64 rows) keeps the first call's choice
     if (a.block_n == 0) {
         a.n2 = 1;
@@ -1304,8 +1236,7 @@ void tc_configure(TcPlan& p, int num_sms) {
         // two N sub-tiles per unit when that makes a multi-wave layer fit in one wave (VGG conv5:
         // 98 -> 49 units on 74 CTA pairs): each A stage then feeds 2 x block_n columns, and with
         // one unit per CTA pair the single 512-column TMEM buffer costs no overlap
-        const char* e = getenv("AI3_N2");
-        const bool n2_ok = !(e && e[0] == '0') && a.cm == CM_BF16 && a.batch == 1 &&
+        const bool n2_ok = knob("AI3_N2", 1) != 0 && a.cm == CM_BF16 && a.batch == 1 &&
                            (a.a_mode == TC_A_IM2COL || a.a_mode == TC_A_TILED2D) && a.out_bf16 && !a.out_nchw &&
                            a.stg_row != 0 && a.Ncols <= 2048 && cg == 2 && a.block_n >= 128 &&
                            a.Ncols % (2 * a.block_n) == 0;
@@ -1318,29 +1249,10 @@ void tc_configure(TcPlan& p, int num_sms) {
     // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
     a.promote_kb = a.cm == CM_3XTF32 ? (256 / (a.row_bytes / 4) > 0 ? 256 / (a.row_bytes / 4) : 1) : 0;
     a.cg = pick_cg(a.M);
-    {
-        const char* e = getenv("AI3_TC_STORE");
-        a.store_mode = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;
-        if (a.store_mode == 0 && !a.bias_smem) a.stg_row = 0;
-    }
-    {
-        const char* e = getenv("AI3_EPI_FAST");
-        a.epi_fast = (e && e[0] == '0') ? 0 : 1;
-    }
-    {
-        const char* e = getenv("AI3_TC_TRACE");
-        a.trace = (e && e[0] == '1') ? 1 : 0;
-    }
-    {
-        const char* e = getenv("AI3_TC_DEBUG");
-        a.dbg = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
-    }
-    if (a.n2 == 2 && ((a.store_mode != 1 && a.store_mode != 3) || !a.epi_fast || a.dbg || a.trace))
-        a.n2 = 1;  // fast epilogue only
-    {
-        const char* e = getenv("AI3_PF");  // L2 prefetch distance in scheduler steps (TILED2D)
-        a.pf_tiles = (e && e[0] >= '0' && e[0] <= '9') ? atoi(e) : 0;
-    }
+    a.epi_fast = knob("AI3_EPI_FAST", 1) != 0;
+    a.trace = knob("AI3_TC_TRACE", 0) != 0;
+    if (a.n2 == 2 && (!a.epi_fast || a.trace)) a.n2 = 1;  // N sub-tiles run in the fast epilogue only
+    a.pf_tiles = knob("AI3_PF", 0);  // L2 prefetch distance in scheduler steps (TILED2D)
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const bool chunked = a.a_mode == TC_A_HALO && a.halo_chunks > 1;
     if (a.a_mode == TC_A_HALO) {
@@ -1374,16 +1286,15 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (chunked) {
         // two halos + as many weight-tap slots as fit, n_stg store buffers per epilogue warp
         {
-            const char* es = getenv("AI3_HALO_NSTG");
-            a.n_stg = (es && (es[0] == '1' || es[0] == '2' || es[0] == '4')) ? es[0] - '0' : 1;
+            const int ns = knob("AI3_HALO_NSTG", 1);
+            a.n_stg = (ns == 1 || ns == 2 || ns == 4) ? ns : 1;
         }
         reserve = fixed + NUM_EPI_WARPS * a.n_stg * 32 * a.stg_row;
         const int tap_bytes = (a.block_n / a.cg) * 128;
-        const char* eh = getenv("AI3_HSLOTS");
-        const char* eb = getenv("AI3_BSLOTS");
-        a.hslots = (eh && atoi(eh) >= 2) ? atoi(eh) : 2;
+        const int kh = knob("AI3_HSLOTS", 2), kb = knob("AI3_BSLOTS", 16);
+        a.hslots = kh >= 2 ? kh : 2;
         int bs = (SMEM_LIMIT - reserve - a.hslots * a.halo_bytes) / tap_bytes;
-        const int bcap = (eb && atoi(eb) >= 2) ? atoi(eb) : 16;  // a deep tap ring hides the weight loads' latency
+        const int bcap = kb >= 2 ? kb : 16;  // a deep tap ring hides the weight loads' latency
         a.bslots = bs > bcap ? bcap : bs;
         a.stages = a.hslots + a.bslots;  // barrier pairs: halo ring, then tap ring
     }
@@ -1416,7 +1327,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     const int max_units = num_sms / a.cg;
     p.grid = (int)(units < max_units ? units : max_units) * a.cg;
     if (p.grid < a.cg) p.grid = a.cg;
-    if (getenv("AI3_TC_VERBOSE")) {  // configuration dump for A/B work (stderr)
+    if (knob("AI3_TC_VERBOSE", 0)) {  // configuration dump for A/B work (stderr)
         fprintf(stderr,
                 "[ai3 tc] mode=%d M=%d N=%d bn=%d cg=%d n2=%d row=%d kb=%d stages=%d n_stg=%d stg_row=%d box64=%d "
                 "n_acc=%d m_tiles=%d n_tiles=%d grid=%d smem=%d\n",
@@ -1427,15 +1338,23 @@ void tc_configure(TcPlan& p, int num_sms) {
 
 cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap* a1, const CUtensorMap* b0,
                       const CUtensorMap* b1, const CUtensorMap* out, cudaStream_t st) {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            SMEM_LIMIT);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
+    // the shared-memory opt-in is a per-device (per-context) attribute: set it once per device
+    static std::mutex mu;
+    static bool opted_in[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!opted_in[dev]) {
+            e = cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+            if (e != cudaSuccess) return e;
+            opted_in[dev] = true;
+        }
+    }
     const CUtensorMap& A1 = a1 ? *a1 : *a0;
     const CUtensorMap& B1 = b1 ? *b1 : *b0;
     const CUtensorMap& O = out ? *out : *a0;  // unused by the kernel unless args.stg_row != 0

@@ -334,6 +334,13 @@ def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None,
                 continue
             replaced.append((node.name, node.target.__name__))
 
+    # fusions below change a module's behaviour, so they only apply to modules called from
+    # exactly one node (a module reused at several call sites keeps its plain semantics)
+    calls = {}
+    for n in graph.nodes:
+        if n.op == "call_module":
+            calls[n.target] = calls.get(n.target, 0) + 1
+
     # fusion: conv2d / linear -> relu (sole consumer) runs as one kernel (fused epilogue)
     def _mod(n):
         return mods.get(n.target) if n.op == "call_module" else None
@@ -346,13 +353,15 @@ def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None,
             continue
         src = node.args[0]
         producer = _mod(src)
-        if isinstance(producer, (Conv2D, L.Linear)) and len(src.users) == 1 and not producer.relu:
+        if isinstance(producer, (Conv2D, L.Linear)) and len(src.users) == 1 and not producer.relu and \
+                calls.get(src.target) == 1:
             producer.relu = True
             node.replace_all_uses_with(src)
             graph.erase_node(node)
             replaced.append((src.name, "fused_relu"))
 
-    # fusion: flatten(NHWC) -> linear reads the activation in place (weight columns permuted once)
+    # fusion: flatten(x, 1) -> linear is one convolution with an H x W kernel over x, which
+    # reads the (NHWC) activation in place (layers.Linear.fused_flatten)
     for node in list(graph.nodes):
         is_flat = (node.op == "call_function" and node.target is L.flatten) or isinstance(_mod(node), L.Flatten)
         if not is_flat or len(node.users) != 1:
@@ -361,7 +370,12 @@ def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None,
         start_dim = node.args[1] if len(node.args) > 1 else node.kwargs.get("start_dim", 1)
         if isinstance(_mod(node), L.Flatten):
             start_dim = _mod(node).start_dim
-        if isinstance(_mod(user), L.Linear) and start_dim == 1 and user.args[0] is node:
+        end_dim = node.args[2] if len(node.args) > 2 else node.kwargs.get("end_dim", -1)
+        if isinstance(_mod(node), L.Flatten):
+            end_dim = _mod(node).end_dim
+        if isinstance(_mod(user), L.Linear) and start_dim == 1 and end_dim == -1 and user.args[0] is node and \
+                calls.get(user.target) == 1:
+            _mod(user).fused_flatten = True
             user.args = (node.args[0],) + tuple(user.args[1:])
             graph.erase_node(node)
             replaced.append((user.name, "flatten_fused"))

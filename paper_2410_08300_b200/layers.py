@@ -169,9 +169,13 @@ class Flatten(nn.Module):
 class Linear(nn.Module):
     """nn.Linear on the tcgen05 engine (ai3_linear_plan_create: a 1x1 convolution).
 
-    ``relu``: fused ReLU epilogue.  ``nhwc_chw``: set by swap_backend when this layer
-    consumes torch.flatten of an NHWC (C, H, W) activation -- the plan then permutes
-    its weight columns once to (H, W, C) order, so the flatten costs nothing.
+    Applies over the last dimension like nn.Linear.  ``relu``: fused ReLU epilogue.
+    ``fused_flatten``: set by swap_backend when this layer's only input is
+    torch.flatten(x, 1) of a 4-D activation.  It then takes that activation (N, C, H, W)
+    itself: flatten -> linear is exactly the convolution of the (C, H, W) map with the
+    weight viewed as (out, C, H, W) and an H x W kernel, so an NHWC activation is read in
+    place and the plan's own weight packing (KCRS -> [K][R][S][C]) does the column
+    reordering -- no transpose pass and no PyTorch data movement.
     """
 
     def __init__(self, orig: nn.Linear, math: str = "strict"):
@@ -180,52 +184,82 @@ class Linear(nn.Module):
         self.in_features, self.out_features = orig.in_features, orig.out_features
         self.math = math
         self.relu = False
+        self.fused_flatten = False
         self._plans = {}
 
-    def _plan(self, batch: int, dtype, device, chw):
-        wv = (self.weight._version, None if self.bias is None else self.bias._version)
-        key = (batch, dtype, device, chw)
+    def _version(self):
+        return (self.weight._version, None if self.bias is None else self.bias._version)
+
+    def _check_dtype(self, x):
+        if self.weight.dtype != x.dtype or (self.bias is not None and self.bias.dtype != x.dtype):
+            raise TypeError(f"ai3 Linear: input dtype {x.dtype} differs from the parameters' {self.weight.dtype} "
+                            "(nn.Linear raises on mixed dtypes too)")
+
+    def _plan(self, batch: int, dtype, device):
+        wv = self._version()
+        key = (batch, dtype, device)
         ent = self._plans.get(key)
         if ent is not None and ent[0] == wv:
             return ent[1]
         lib = _lib.load()
-        w = self.weight.detach().to(device=device, dtype=dtype)
-        if chw is not None:  # columns (c, h, w) -> (h, w, c): swap-time parameter layout, once per plan
-            C, H, W = chw
-            w = w.view(self.out_features, C, H, W).permute(0, 2, 3, 1)
+        w = self.weight.detach()
+        b = None if self.bias is None else self.bias.detach()
+        if w.device != device:
+            raise ValueError("ai3 Linear: parameters and input on different devices")
         w = w.contiguous()
-        b = None if self.bias is None else self.bias.detach().to(device=device, dtype=dtype).contiguous()
+        b = None if b is None else b.contiguous()
         nbytes = ctypes.c_size_t()
         _check(lib.ai3_linear_plan_weight_bytes(batch, self.in_features, self.out_features, int(b is not None),
                                                 _dtype_id(dtype), _math_id(self.math), ctypes.byref(nbytes)))
         wbuf = torch.empty(max(nbytes.value, 256), dtype=torch.uint8, device=device)
         h = ctypes.c_void_p()
-        with torch.cuda.device(device):
-            _check(lib.ai3_linear_plan_create(batch, self.in_features, self.out_features, _dtype_id(dtype),
-                                              _math_id(self.math), w.data_ptr(),
-                                              None if b is None else b.data_ptr(), wbuf.data_ptr(), wbuf.numel(),
-                                              _stream_ptr(device), ctypes.byref(h)))
-            if self.relu:
-                _check(lib.ai3_conv2d_plan_set_relu(h, 1))
+        _check(lib.ai3_linear_plan_create(batch, self.in_features, self.out_features, _dtype_id(dtype),
+                                          _math_id(self.math), w.data_ptr(), None if b is None else b.data_ptr(),
+                                          wbuf.data_ptr(), wbuf.numel(), _stream_ptr(device), ctypes.byref(h)))
+        if self.relu:
+            _check(lib.ai3_conv2d_plan_set_relu(h, 1))
         plan = _LinearPlan(h, wbuf, (w, b), int(lib.ai3_conv2d_plan_workspace_size(h)))
         self._plans[key] = (wv, plan)
         return plan
 
+    def _flatten_plan(self, x):
+        """flatten(x, 1) -> linear as one convolution with an H x W kernel (see class doc)."""
+        from .conv import ConvPlan
+        N, C, H, W = (int(v) for v in x.shape)
+        if C * H * W != self.in_features:
+            raise ValueError(f"ai3 Linear: flatten of {tuple(x.shape)} gives {C * H * W} features, "
+                             f"the layer takes {self.in_features}")
+        lay = layout_of(x)
+        key = ("flatten", tuple(x.shape), x.dtype, x.device, lay)
+        wv = self._version()
+        ent = self._plans.get(key)
+        if ent is None or ent[0] != wv:
+            w4 = self.weight.detach().view(self.out_features, C, H, W)  # a view: no data moves
+            plan = ConvPlan(w4, self.bias, x.shape, 1, 0, 1, 1, "implicit_gemm", self.math, in_layout=lay,
+                            out_layout=_lib.NHWC)
+            if self.relu:
+                plan.set_relu(True)
+            ent = (wv, plan)
+            self._plans[key] = ent
+        return ent[1]
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         _require_cuda(x)
-        chw = None
-        if x.dim() == 4:
-            if layout_of(x) == _lib.NHWC and not x.is_contiguous():
-                chw = tuple(int(v) for v in x.shape[1:])  # flatten(NHWC) fused: read the buffer as is
-            else:
-                x = torch.flatten(x, 1)
-        if chw is None:
-            if x.dim() != 2:
-                lead = x.shape[:-1]
-                return self.forward(x.reshape(-1, x.shape[-1])).reshape(*lead, self.out_features)
-            x = x.contiguous()
+        self._check_dtype(x)
+        if self.fused_flatten:
+            if x.dim() == 4:
+                y = self._flatten_plan(x)(x)  # (N, out, 1, 1), NHWC == (N, out) row-major
+                return y.view(x.shape[0], self.out_features)
+            x = flatten(x, 1)
+        if x.shape[-1] != self.in_features:
+            raise ValueError(f"ai3 Linear: input has {x.shape[-1]} features in its last dimension, "
+                             f"the layer takes {self.in_features}")
+        if x.dim() != 2:
+            lead = x.shape[:-1]
+            return self.forward(x.reshape(-1, x.shape[-1])).reshape(*lead, self.out_features)
+        x = x.contiguous()
         batch = x.shape[0]
-        plan = self._plan(batch, x.dtype, x.device, chw)
+        plan = self._plan(batch, x.dtype, x.device)
         y = torch.empty((batch, self.out_features), dtype=x.dtype, device=x.device)
         ws = _WS.get(x.device, plan.ws_bytes)
         _check(_lib.load().ai3_conv2d_plan_execute(plan.h, x.data_ptr(), y.data_ptr(),
@@ -243,18 +277,3 @@ class _LinearPlan:
         if self.h is not None and _lib._lib is not None:
             _lib._lib.ai3_conv2d_plan_destroy(self.h)
             self.h = None
-
-
-class FlattenLinear(nn.Module):
-    """torch.flatten followed by an ai3 Linear that is its only consumer: the Linear reads
-    the NHWC activation directly (weight columns permuted once), no transpose pass."""
-
-    def __init__(self, linear: Linear, start_dim: int = 1):
-        super().__init__()
-        self.linear = linear
-        self.start_dim = start_dim
-
-    def forward(self, x):
-        if x.dim() == 4 and self.start_dim == 1:
-            return self.linear(x)
-        return self.linear(flatten(x, self.start_dim))

@@ -90,7 +90,11 @@ def max_over_ranks(value: float, device) -> float:
     return float(t.item())
 
 
-def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check: bool, swap: str = "backend"):
+def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check: bool, swap: str = "backend",
+        quiet: bool = False, finalize: bool = True, cuda_graph: bool = False):
+    """Run BASELINE configs[4] on this rank's slab; returns the result dict (rank 0 prints it
+    unless quiet).  finalize=False leaves the process group up (bench.py calls this inside
+    its own run)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -101,6 +105,8 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
     lo, hi = shard_bounds(global_batch, world, rank)
     x = make_images(lo, hi, seed + 1, device)
     model = build_vgg16(device, algo=algo, seed=seed, swap=swap)
+    if cuda_graph and swap == "backend":
+        model.cuda_graph = True
     with torch.inference_mode():
         for _ in range(warmup):
             y = model(x)
@@ -116,15 +122,19 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
     ms = s.elapsed_time(e) / steps
     if world > 1:
         ms = max_over_ranks(ms, device)
-    result = {"global_batch": global_batch, "n_gpus": world, "ms_per_forward": ms,
-              "images_per_s": global_batch / (ms * 1e-3), "algo": algo, "swap": swap}
+    result = {"global_batch": global_batch, "n_gpus": world, "images_per_rank": hi - lo, "ms_per_forward": ms,
+              "images_per_s": global_batch / (ms * 1e-3), "algo": algo, "swap": swap,
+              "timing": "CUDA events around the forward on every rank, max over ranks; the all-gather is "
+                        "timed separately and excluded"}
     if world > 1:
         counts = [shard_bounds(global_batch, world, r)[1] - shard_bounds(global_batch, world, r)[0]
                   for r in range(world)]
+        torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         logits = gather_rows(y.float(), world, counts)
         torch.cuda.synchronize(device)
         result["gather_ms"] = (time.perf_counter() - t0) * 1e3
+        result["gathered_rows"] = int(logits.shape[0])
     else:
         logits = y.float()
     if check:
@@ -145,9 +155,9 @@ def run(global_batch: int, algo: str, steps: int, warmup: int, seed: int, check:
             dist.all_reduce(flags[1:], op=dist.ReduceOp.MAX)
         result["logits_bit_identical_when_sharded"] = bool(flags[0].item() == 1.0)
         result["logits_max_abs_diff_vs_single_image"] = float(flags[1].item())
-    if rank == 0:
+    if rank == 0 and not quiet:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if world > 1 and finalize:
         dist.destroy_process_group()
     return result
 

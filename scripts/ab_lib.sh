@@ -4,7 +4,7 @@ OLD="$1"; shift
 for rep in 1 2; do
   for lib in "$OLD" paper_2410_08300_b200/libai3.so; do
     for l in ${LAYERS:-conv1_2 conv3_2 conv5_2}; do
-      AI3_LIB=$lib timeout 60 python scripts/layer_bench.py $l implicit_gemm --reps 20 | sed "s|^|[$(basename $lib)] |"
+      timeout 60 python scripts/layer_bench.py $l implicit_gemm --reps 20 --lib $lib | sed "s|^|[$(basename $lib)] |"
     done
   done
 done

@@ -4,7 +4,6 @@ import argparse, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
-import paper_2410_08300_b200 as ai3
 from synth import workload, conv_inputs
 
 ap = argparse.ArgumentParser()
@@ -14,7 +13,12 @@ ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--net", default="vgg16")
 ap.add_argument("--dtype", default="bf16")
+ap.add_argument("--lib", default=None, help="library to load (e.g. paper_2410_08300_b200/libai3_dev.so for knobs)")
 a = ap.parse_args()
+if a.lib:
+    from paper_2410_08300_b200 import _lib
+    _lib.select_library(a.lib)
+import paper_2410_08300_b200 as ai3
 spec = [l for l in workload(a.net, a.batch) if l.name == a.layer][0]
 dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
 x = torch.randn(spec.N, spec.C, spec.H, spec.W, device="cuda").to(dt).contiguous(memory_format=torch.channels_last)

@@ -23,3 +23,19 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"] == "vgg16_conv_stack"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_launches_n_ranks_itself():
+    """`bench.py --gpus 2` without a torchrun environment launches the two ranks itself (one
+    process per device, torch.distributed.run on 127.0.0.1); the plumbing is checked here with
+    gloo (--launch-check): both ranks join, the max-over-ranks reduction sees rank 1, and
+    rank 0 alone prints one line with n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["max_rank"] == 1.0 and d["ranks_mask"] == 3

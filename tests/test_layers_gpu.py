@@ -128,17 +128,38 @@ def test_linear(dtype, math, shape):
     assert _rel(_host(m(xt))[rows], oops.relu(ref)) <= TOL[(dtype, math)]
 
 
+@pytest.mark.parametrize("nhwc", [True, False])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_flatten_linear_fused_nhwc(dtype):
-    """flatten(NHWC) -> Linear: the plan reads the channels_last buffer with permuted weights."""
+def test_flatten_linear_fused(dtype, nhwc):
+    """flatten -> Linear fused: one convolution with a 7x7 kernel over the (C, 7, 7) map; the
+    activation is read in place (NHWC or NCHW) and the plan's weight packing reorders columns."""
     import paper_2410_08300_b200.layers as L
     rng = np.random.default_rng(11)
-    x = _dev(rng.standard_normal((4, 32, 7, 7)), dtype, nhwc=True)
+    x = _dev(rng.standard_normal((4, 32, 7, 7)), dtype, nhwc=nhwc)
     lin = nn.Linear(32 * 49, 40).cuda().to(x.dtype)
-    fl = L.FlattenLinear(L.Linear(lin))
+    fl = L.Linear(lin)
+    fl.fused_flatten = True
     y = _host(fl(x))
     ref = oops.linear(oops.flatten(_host(x)), _host(lin.weight), _host(lin.bias))
+    assert y.shape == (4, 40)
     assert _rel(y, ref) <= TOL[(dtype, "strict")]
+
+
+def test_linear_last_dim_and_checks():
+    """nn.Linear semantics: a 4-D input is transformed over its last dimension; a wrong
+    feature count or dtype raises instead of reading out of bounds."""
+    import paper_2410_08300_b200.layers as L
+    rng = np.random.default_rng(12)
+    lin = nn.Linear(16, 24).cuda()
+    m = L.Linear(lin)
+    x = _dev(rng.standard_normal((2, 3, 5, 16)), "f32")
+    y = _host(m(x))
+    ref = oops.linear(_host(x).reshape(-1, 16), _host(lin.weight), _host(lin.bias)).reshape(2, 3, 5, 24)
+    assert _rel(y, ref) <= TOL[("f32", "strict")]
+    with pytest.raises(ValueError):
+        m(_dev(rng.standard_normal((4, 15)), "f32"))
+    with pytest.raises(TypeError):
+        m(_dev(rng.standard_normal((4, 16)), "bf16"))
 
 
 @pytest.mark.parametrize("algo", ["implicit_gemm", "gemm", "direct", "winograd", "smm", "kn2row"])

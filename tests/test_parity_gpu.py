@@ -172,15 +172,7 @@ def test_deterministic_and_batch_independent(algo):
         assert torch.equal(part, y1[s:s + 2])
 
 
-# ------------------------------------------------------------------ the harness has teeth
-def test_mutation_dropped_bias_is_caught():
-    shape = ConvShape("mut", 2, 16, 12, 12, 24, 3, 3, 1, 1)
-    x, w, b = inputs(shape, 9, "f32")
-    y = run_ai3(shape, x, w, b, "implicit_gemm", "f32", "strict", "nchw")
-    r = ref(shape, x, w, b)
-    mutated = y - b.astype(np.float64)[None, :, None, None]
-    assert oracle.rel_err(y, r) <= 1e-5
-    assert oracle.rel_err(mutated, r) > 1e-3
+# (the harness has teeth: tests/test_mutation_gpu.py runs it against a faulty build)
 
 
 def test_errors_surface_as_exceptions():

@@ -76,18 +76,3 @@ def test_s2d_integer_stem_bit_exact(dtype, math):
     r = oracle.conv2d(x, w, b, 2, 3, 1, 1)
     assert np.abs(r).max() < (256 if small else 2 ** 24)
     np.testing.assert_array_equal(y, r)
-
-
-@pytest.mark.parametrize("env", [("AI3_HALO32_SW", "1"), ("AI3_S2D_SPLIT", "0"), ("AI3_S2D_C64", "0"), ("AI3_TC_STORE", "3")],
-                         ids=lambda e: e[0])
-@pytest.mark.parametrize("case", [CASES[0], CASES[1], CASES[-3]], ids=lambda c: c[0])
-def test_s2d_alternative_layouts(case, env, monkeypatch):
-    """The A/B switches of the 32-byte halo (one SWIZZLE_32B box; plane-split s2d rows) and of
-    the s2d channel padding stay parity-green (they are read when a plan is laid out)."""
-    monkeypatch.setenv(*env)
-    name, N, C, H, W, K, R, S, st, pd = case
-    shape = ConvShape(name, N, C, H, W, K, R, S)
-    x, w, b = conv_inputs(shape, seed=stable_seed((name, env)), dtype="bf16")
-    y = _run(x, w, b, st, pd, "bf16", "strict", "nhwc")
-    r = oracle.conv2d(x, w, b, st, pd, 1, 1)
-    assert oracle.rel_err(y, r) <= TOL[("bf16", "strict")]
