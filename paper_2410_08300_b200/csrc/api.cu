@@ -282,6 +282,8 @@ struct ai3_plan {
     CUtensorMap tout{};
     int launches = 1;
     int relu = 0;  // fused ReLU epilogue (ai3_conv2d_plan_set_relu)
+    bool kn_inplace = false;  // kn2row: fp32 NHWC output accumulates in y itself (no workspace)
+    int kn_first = -1;        // kn2row: a tap covering every output pixel (runs first, writes), or -1
 };
 
 namespace {
@@ -309,6 +311,10 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     pl.pb = c;
     pl.algo = algo;
     pl.cm = compute_mode(c);
+    // Winograd under `tf32`: the transforms amplify TF32 operand rounding past the 1e-3 bound
+    // (measured 1.04e-3 on VGG conv1_1, C = 3), so its transformed-domain GEMM keeps the
+    // fp32-accurate 3xTF32 split (R25)
+    if (algo == AI3_ALGO_WINOGRAD && pl.cm == CM_TF32) pl.cm = CM_3XTF32;
     pl.elem = cm_elem_bytes(pl.cm);
     pl.splits = cm_splits(pl.cm);
     pl.bias_present = c.has_bias;
@@ -462,18 +468,32 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.num_kb = (int)((kred * pl.elem + a.row_bytes - 1) / a.row_bytes);
         pl.launches = 2;  // im2col + GEMM
     } else if (algo == AI3_ALGO_KN2ROW) {
-        // one GEMM over every input pixel: Z[N*H*W][R*S*K] (fp32 partial planes), then shift-accumulate
+        // one GEMM per filter tap over every input pixel, its epilogue shift-accumulating into
+        // the fp32 accumulator [N*P*Q][K] (kn2row.cu); fp32 NHWC outputs accumulate in place
         const int64_t Mz = c.N * c.H * c.W;
+        pl.kn_inplace = c.dtype == AI3_F32 && c.out_layout == AI3_NHWC;
         pl.ws_M = ws;
-        ws = align_up(ws + (size_t)Mz * c.R * c.S * c.K * 4);
+        if (!pl.kn_inplace) ws = align_up(ws + (size_t)c.N * c.P * c.Q * c.K * 4);
         a.a_mode = TC_A_TILED2D;
         a.M = (int)Mz;
-        a.Ncols = (int)(c.R * c.S * c.K);
+        a.Ncols = (int)c.K;
         a.row_bytes = tiled_row_bytes(pl.Cpad * pl.elem);
         a.num_kb = (int)((pl.Cpad * pl.elem + a.row_bytes - 1) / a.row_bytes);
         a.out_bf16 = 0;
         a.out_nchw = 0;
-        pl.launches = (pl.need_prep ? 1 : 0) + 2;
+        a.kn = 1;
+        a.kn_H = (int)c.H; a.kn_W = (int)c.W;
+        a.P = (int)c.P; a.Q = (int)c.Q; a.sh = c.sh; a.sw = c.sw;
+        // a tap that reaches every output pixel runs first and writes instead of accumulating
+        // (no zero-fill pass); VGG's 3x3 / pad 1 convs have one, the centre tap
+        pl.kn_first = -1;
+        for (int64_t t = 0; t < c.R * c.S && pl.kn_first < 0; ++t) {
+            const int64_t r = t / c.S, sx = t % c.S;
+            const int64_t h0 = -c.ph + r * c.dh, h1 = (c.P - 1) * c.sh - c.ph + r * c.dh;
+            const int64_t w0 = -c.pw + sx * c.dw, w1 = (c.Q - 1) * c.sw - c.pw + sx * c.dw;
+            if (h0 >= 0 && h1 < c.H && w0 >= 0 && w1 < c.W) pl.kn_first = (int)t;
+        }
+        pl.launches = (pl.need_prep ? 1 : 0) + (int)(c.R * c.S) + 1;
     } else {  // WINOGRAD
         const int64_t T = c.N * ((c.P + 1) / 2) * ((c.Q + 1) / 2);
         pl.ws_V = ws;
@@ -495,7 +515,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     pl.ws_bytes = ws;
     // TMA-store epilogue for row-major (NHWC / [b][T][K]) outputs whose rows are 16-byte multiples
     const int eo = a.out_bf16 ? 2 : 4;
-    a.stg_row = (!a.out_nchw && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
+    a.stg_row = (!a.out_nchw && !a.kn && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
     a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD && algo != AI3_ALGO_KN2ROW) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
@@ -758,9 +778,34 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.out = y;
     } else if (pl.algo == AI3_ALGO_KN2ROW) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
-        tp.args.out = w + pl.ws_M;
+        if (pl.kn_inplace && !aligned(y, 16))
+            return fail(AI3_ERR_INVALID_ARGUMENT, "kn2row: y must be 16-byte aligned (fp32 NHWC accumulates in place)");
+        float* acc = pl.kn_inplace ? reinterpret_cast<float*>(y) : reinterpret_cast<float*>(w + pl.ws_M);
+        tp.args.out = acc;
         tp.args.bias = nullptr;
         tp.args.relu = 0;
+        if (pl.kn_first < 0) {  // no tap reaches every output pixel: start from zero
+            e = cudaMemsetAsync(acc, 0, (size_t)c.N * c.P * c.Q * c.K * 4, st);
+            if (e != cudaSuccess) return cuda_fail(e, "kn2row accumulator fill");
+        }
+        const int taps = (int)(c.R * c.S);
+        for (int i = 0; i < taps; ++i) {  // fixed tap order: deterministic sums
+            const int t = pl.kn_first < 0 ? i : (i == 0 ? pl.kn_first : (i <= pl.kn_first ? i - 1 : i));
+            const int r = t / (int)c.S, sx = t % (int)c.S;
+            TcPlan tt = tp;
+            tt.args.kn = (pl.kn_first >= 0 && i == 0) ? 2 : 1;
+            tt.args.b_row_off = t * (int)c.K;
+            tt.args.kn_oh = c.ph - r * c.dh;
+            tt.args.kn_ow = c.pw - sx * c.dw;
+            e = launch_tc(tt, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, nullptr, st);
+            if (e != cudaSuccess) return cuda_fail(e, "kn2row tap GEMM launch");
+        }
+        if (!pl.kn_inplace || bias || pl.relu) {
+            e = launch_kn2row_finalize(acc, bias, y, c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q,
+                                       pl.relu, st);
+            if (e != cudaSuccess) return cuda_fail(e, "kn2row finalize launch");
+        }
+        return ok();
     } else if (pl.algo == AI3_ALGO_GEMM) {
         e = launch_im2col(x, c.in_layout, c.dtype, c.N, c.C, c.H, c.W, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw, c.ph,
                           c.pw, c.dh, c.dw, pl.Kp, pl.cm, w + pl.ws_A, w + pl.ws_Alo, st);
@@ -786,12 +831,6 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
     e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
-    if (pl.algo == AI3_ALGO_KN2ROW) {
-        e = launch_kn2row_accumulate(reinterpret_cast<const float*>(w + pl.ws_M), bias, y, c.out_layout == AI3_NHWC,
-                                     c.dtype == AI3_BF16, c.N, c.H, c.W, c.K, c.P, c.Q, (int)c.R, (int)c.S, c.sh, c.sw,
-                                     c.ph, c.pw, c.dh, c.dw, pl.relu, st);
-        if (e != cudaSuccess) return cuda_fail(e, "kn2row shift-accumulate launch");
-    }
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,
                                    c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);
@@ -952,7 +991,12 @@ ai3_algo ai3_conv2d_plan_algo(const ai3_plan* plan) { return plan ? plan->algo :
 
 size_t ai3_conv2d_plan_workspace_size(const ai3_plan* plan) { return plan ? plan->ws_bytes : 0; }
 
-int ai3_conv2d_plan_num_launches(const ai3_plan* plan) { return plan ? plan->launches : 0; }
+int ai3_conv2d_plan_num_launches(const ai3_plan* plan) {
+    if (!plan) return 0;
+    if (plan->algo == AI3_ALGO_KN2ROW && plan->kn_inplace && !plan->bias_present && !plan->relu)
+        return plan->launches - 1;  // fp32 NHWC, no bias, no ReLU: the taps write the output, no finalize
+    return plan->launches;
+}
 
 ai3_status ai3_conv2d_plan_execute(ai3_plan* plan, const void* x, void* y, void* workspace, size_t workspace_bytes,
                                    void* stream) {

@@ -115,10 +115,10 @@ cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st);
 // KCRS -> [(r*S+s)*K + k][Cpad] rows, compute mode (+ lo).
 cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
                                        int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
-// Z fp32 [N*H*W][R*S*K] -> y (+bias): shift-accumulate of the R*S partial planes.
-cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
-                                     int64_t H, int64_t W, int64_t K, int64_t P, int64_t Q, int R, int S, int sh,
-                                     int sw, int ph, int pw, int dh, int dw, int relu, cudaStream_t st);
+// acc fp32 [N*P*Q][K] (the taps' shift-accumulated sums) -> y (+bias, ReLU, cast to y's
+// dtype and layout).  acc == y (fp32 NHWC output accumulated in place) is allowed.
+cudaError_t launch_kn2row_finalize(const float* acc, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
+                                   int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st);
 
 // ---------------------------------------------------------------- im2col / winograd transforms
 // raw x (NCHW|NHWC, dtype) -> A[M][Kp] in compute mode (+ lo), columns (r, s, c) over the
@@ -183,6 +183,12 @@ struct TcArgs {
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int relu;       // 1: fused ReLU after the bias (model path)
     int pf_tiles;   // TILED2D: prefetch the A panel of the tile this many scheduler steps ahead into L2 (0 = off)
+    // kn2row tap epilogue (a_mode TILED2D over the input pixels [N*H*W][Cpad], one launch per
+    // filter tap): row m = input pixel (n, h, w) adds its K partial sums into the fp32 output
+    // accumulator `out` [N*P*Q][K] at output pixel p = (h + kn_oh) / sh, q = (w + kn_ow) / sw
+    // when both divide and land inside P x Q.  kn = 0 off; 1 read-add-write; 2 write (the
+    // first tap, when it covers every output pixel).  b_row_off: first B row of this tap.
+    int kn, kn_H, kn_W, kn_oh, kn_ow, b_row_off;
     int n2;         // N sub-tiles per unit (1, or 2: one A stage feeds two block_n-column MMAs --
                     // for single-wave layers; bf16 im2col / tiled with the fast epilogue only)
     // gather mode (a_mode == TC_A_GATHER, implicit_precomp_gemm): precomputed input-row table

@@ -3,19 +3,22 @@
 // multiplication but differs in that it transforms the kernel into row vectors in
 // order to decrease memory usage").
 //
-// The R*S filter taps become R*S 1x1 convolutions, i.e. the kernel is laid out as
-// R*S*K rows of C weights and ONE tcgen05 GEMM over the (unpadded, unstrided) input
-// pixels computes every tap's partial plane at once:
+// The R*S filter taps become R*S 1x1 convolutions: the kernel is laid out as R*S*K rows of
+// C weights (pack below), and for every tap (r, s) one tcgen05 GEMM over the (unpadded,
+// unstrided) input pixels computes that tap's partial plane
 //
-//   Z[n,h,w][(r*S + s)*K + k] = sum_c x[n,c,h,w] * w[k,c,r,s]          (tc_engine.cu)
+//   Z_rs[n,h,w][k] = sum_c x[n,c,h,w] * w[k,c,r,s]                       (tc_engine.cu)
 //
-// and the shift-accumulate pass adds the taps' planes at their offsets:
+// whose epilogue shift-accumulates it straight into ONE fp32 output accumulator
+// (tc_engine.cu kn2row_store; no partial plane is ever stored):
 //
-//   y[n,k,p,q] = b[k] + sum_{r,s} Z[n, p*sh - ph + r*dh, q*sw - pw + s*dw][(r*S+s)*K + k]
+//   acc[n,p,q][k] += Z_rs[n, p*sh - ph + r*dh, q*sw - pw + s*dw][k]
 //
-// with out-of-image taps contributing zero.  Partial sums are computed at unit-stride
-// resolution and subsampled by the stride (the SPEC.md:204 reading).  The input is
-// never replicated (im2col's R*S-fold copy); the price is the fp32 partial planes Z.
+// (input pixels off the strided output grid, and out-of-image taps, contribute nothing:
+// the SPEC.md:204 reading).  A finalize pass adds the bias and casts (kernel below).  Extra
+// memory is the accumulator, O(N*K*P*Q) -- none at all for fp32 NHWC outputs, which
+// accumulate in place -- against im2col's R*S-fold copy of the input: the memory saving
+// PAPER.md:54 names.  Taps run in a fixed order, so results are deterministic.
 #include <algorithm>
 #include <cuda_bf16.h>
 #include "internal.h"
@@ -61,74 +64,62 @@ cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K
     return cudaGetLastError();
 }
 
-// One thread per (output pixel, VK consecutive output channels): VK-wide loads of the
-// R*S partial rows (consecutive threads read consecutive channels of one row).
-// IDX: uint32_t when the thread count fits (64-bit divisions would dominate this HBM-bound pass).
-template <int VK, typename IDX>
-__global__ void kn2row_accumulate_kernel(const float* __restrict__ Z, const float* __restrict__ bias, void* y,
-                                         int out_nhwc, int bf16, int64_t N, int64_t H, int64_t W, int64_t K,
-                                         int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh,
-                                         int dw, int relu) {
-    const IDX kg = (IDX)(K / VK);
-    const IDX total = (IDX)(N * P * Q * (int64_t)kg);
-    const int64_t zrow = (int64_t)R * S * K;
-    const IDX Qi = (IDX)Q, Pi = (IDX)P;
-    for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
-        const IDX mi = i / kg;
-        const int64_t k0 = (int64_t)(i - mi * kg) * VK;
-        const int64_t m = mi;
-        const IDX mq = mi / Qi;
-        const int64_t q = mi - mq * Qi, p = mq % Pi, n = mq / Pi;
-        float acc[VK];
+// acc fp32 [N*P*Q][K] -> y: + bias, ReLU, cast, NHWC (4 channels per thread, 16-byte loads) or
+// NCHW.  acc may alias y (fp32 NHWC output accumulated in place).
+template <int VK>
+__global__ void kn2row_finalize_kernel(const float* acc, const float* __restrict__ bias, void* y, int out_nhwc,
+                                       int bf16, uint32_t PQ, uint32_t K, uint64_t total_groups, int relu) {
+    const uint32_t kg = K / VK;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total_groups;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t m = i / kg;
+        const uint32_t k0 = (uint32_t)(i - m * kg) * VK;
+        float v[VK];
+        if (VK == 4) {
+            const float4 a4 = *reinterpret_cast<const float4*>(acc + m * K + k0);
+            v[0] = a4.x; v[1] = a4.y; v[2 % VK] = a4.z; v[3 % VK] = a4.w;
+        } else {
 #pragma unroll
-        for (int v = 0; v < VK; ++v) acc[v] = 0.f;
-        for (int r = 0; r < R; ++r) {
-            const int64_t ih = p * sh - ph + (int64_t)r * dh;
-            if (ih < 0 || ih >= H) continue;
-            for (int s = 0; s < S; ++s) {
-                const int64_t iw = q * sw - pw + (int64_t)s * dw;
-                if (iw < 0 || iw >= W) continue;
-                const float* src = Z + ((n * H + ih) * W + iw) * zrow + (int64_t)(r * S + s) * K + k0;
-                if (VK == 4) {
-                    const float4 z = *reinterpret_cast<const float4*>(src);
-                    acc[0] += z.x; acc[1] += z.y; acc[2] += z.z; acc[3] += z.w;
-                } else {
-#pragma unroll
-                    for (int v = 0; v < VK; ++v) acc[v] += src[v];
-                }
-            }
+            for (int j = 0; j < VK; ++j) v[j] = acc[m * K + k0 + j];
         }
 #pragma unroll
-        for (int v = 0; v < VK; ++v) {
-            const int64_t k = k0 + v;
-            float val = acc[v] + (bias ? bias[k] : 0.f);
-            if (relu && val < 0.f) val = 0.f;
-            const int64_t o = out_nhwc ? m * K + k : ((n * K + k) * P + p) * Q + q;
-            if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(val);
-            else reinterpret_cast<float*>(y)[o] = val;
+        for (int j = 0; j < VK; ++j) {
+            if (bias) v[j] += bias[k0 + j];
+            if (relu && v[j] < 0.f) v[j] = 0.f;  // NaN passes (torch.relu)
+        }
+        if (out_nhwc) {
+            if (bf16) {
+#pragma unroll
+                for (int j = 0; j < VK; ++j) reinterpret_cast<__nv_bfloat16*>(y)[m * K + k0 + j] = __float2bfloat16_rn(v[j]);
+            } else if (VK == 4) {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + m * K + k0) = make_float4(v[0], v[1 % VK], v[2 % VK], v[3 % VK]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < VK; ++j) reinterpret_cast<float*>(y)[m * K + k0 + j] = v[j];
+            }
+        } else {
+            const uint64_t n = m / PQ, pq = m - n * PQ;
+#pragma unroll
+            for (int j = 0; j < VK; ++j) {
+                const uint64_t o = (n * K + k0 + j) * PQ + pq;
+                if (bf16) reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(v[j]);
+                else reinterpret_cast<float*>(y)[o] = v[j];
+            }
         }
     }
 }
 
-cudaError_t launch_kn2row_accumulate(const float* Z, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
-                                     int64_t H, int64_t W, int64_t K, int64_t P, int64_t Q, int R, int S, int sh,
-                                     int sw, int ph, int pw, int dh, int dw, int relu, cudaStream_t st) {
+cudaError_t launch_kn2row_finalize(const float* acc, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
+                                   int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st) {
     const int VK = K % 4 == 0 ? 4 : 1;
-    const int64_t total = N * P * Q * (K / VK);
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    const bool small = total < (1LL << 31);
-    if (VK == 4 && small)
-        kn2row_accumulate_kernel<4, uint32_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
-                                                                    sh, sw, ph, pw, dh, dw, relu);
-    else if (VK == 4)
-        kn2row_accumulate_kernel<4, int64_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
-                                                                   sh, sw, ph, pw, dh, dw, relu);
-    else if (small)
-        kn2row_accumulate_kernel<1, uint32_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
-                                                                    sh, sw, ph, pw, dh, dw, relu);
+    const uint64_t groups = (uint64_t)(N * P * Q) * (uint64_t)(K / VK);
+    const int grid = (int)std::min<uint64_t>((groups + 255) / 256, 148 * 16);
+    if (VK == 4)
+        kn2row_finalize_kernel<4><<<grid, 256, 0, st>>>(acc, bias, y, out_nhwc, bf16, (uint32_t)(P * Q), (uint32_t)K,
+                                                        groups, relu);
     else
-        kn2row_accumulate_kernel<1, int64_t><<<grid, 256, 0, st>>>(Z, bias, y, out_nhwc, bf16, N, H, W, K, P, Q, R, S,
-                                                                   sh, sw, ph, pw, dh, dw, relu);
+        kn2row_finalize_kernel<1><<<grid, 256, 0, st>>>(acc, bias, y, out_nhwc, bf16, (uint32_t)(P * Q), (uint32_t)K,
+                                                        groups, relu);
     return cudaGetLastError();
 }
 

@@ -123,6 +123,42 @@ __device__ __forceinline__ void epilogue_store(const TcArgs& a, float (&f)[32], 
     }
 }
 
+// kn2row tap epilogue (TcArgs::kn): this lane's row m is input pixel (n, h, w); its 32 partial
+// sums (columns col0..col0+31) go to output pixel ((h + kn_oh) / sh, (w + kn_ow) / sw) of the
+// fp32 accumulator when that lands on the output grid (each input pixel feeds at most one
+// output pixel per tap, so one launch never writes an element twice: no atomics).
+__device__ __forceinline__ void kn2row_store(const TcArgs& a, const float (&f)[32], int m, int col0) {
+    if (col0 >= a.Ncols || m >= a.M) return;
+    const int hw = a.kn_H * a.kn_W;
+    const int n = m / hw;
+    const int rem = m - n * hw;
+    const int h = rem / a.kn_W, w = rem - (rem / a.kn_W) * a.kn_W;
+    const int pn = h + a.kn_oh, qn = w + a.kn_ow;
+    if (pn < 0 || qn < 0) return;
+    const int p = pn / a.sh, q = qn / a.sw;
+    if (p * a.sh != pn || q * a.sw != qn || p >= a.P || q >= a.Q) return;
+    float* dst = reinterpret_cast<float*>(a.out) + (((int64_t)n * a.P + p) * a.Q + q) * a.Ncols + col0;
+    if (col0 + 32 <= a.Ncols && (a.Ncols % 4) == 0) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        if (a.kn == 2) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d4[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+        } else {
+            float4 old[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) old[j] = d4[j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                d4[j] = make_float4(old[j].x + f[4 * j], old[j].y + f[4 * j + 1], old[j].z + f[4 * j + 2],
+                                    old[j].w + f[4 * j + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (col0 + j < a.Ncols) dst[j] = a.kn == 2 ? f[j] : dst[j] + f[j];
+    }
+}
+
 // ---------------------------------------------------------------- TMA producer (one thread)
 // Walks the K-blocks of every tile of this CTA group and streams A/B tiles into the smem
 // ring.  Filter-tap / channel-chunk coordinates advance incrementally (no division in
@@ -201,8 +237,8 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
                 } else if (a.a_mode == TC_A_TILED2D) {
                     tma_load_2d(sA, &ta0, bar, kx, m0);
                     if (splits == 2) tma_load_2d(sA + a_bytes, &ta1, bar, kx, m0);
-                    tma_load_2d(sB, &tb0, bar, kx, n0);
-                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, bar, kx, n0);
+                    tma_load_2d(sB, &tb0, bar, kx, n0 + a.b_row_off);
+                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, bar, kx, n0 + a.b_row_off);
                 } else {
                     tma_load_3d(sA, &ta0, bar, kx, m0, b);
                     if (splits == 2) tma_load_3d(sA + a_bytes, &ta1, bar, kx, m0, b);
@@ -221,8 +257,8 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
                 } else if (a.a_mode == TC_A_TILED2D) {
                     tma_load_2d_cg2(sA, &ta0, bar, kx, m0);
                     if (splits == 2) tma_load_2d_cg2(sA + a_bytes, &ta1, bar, kx, m0);
-                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0);
-                    if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kx, n0);
+                    tma_load_2d_cg2(sB, &tb0, bar, kx, n0 + a.b_row_off);
+                    if (splits == 2) tma_load_2d_cg2(sB + b_bytes, &tb1, bar, kx, n0 + a.b_row_off);
                 } else {
                     tma_load_3d_cg2(sA, &ta0, bar, kx, m0, b);
                     if (splits == 2) tma_load_3d_cg2(sA + a_bytes, &ta1, bar, kx, m0, b);
@@ -1000,7 +1036,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];
             }
             if (a.stg_row == 0) {
-                if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
+                if (a.kn) kn2row_store(a, f, m_row0 + lane, col0);
+                else if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
                 return;
             }
             // box64: bf16 rows of 64 channels (128 B) per TMA store -- two 32-column chunks share

@@ -186,3 +186,28 @@ def test_product_never_imports_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), fn
+
+
+def test_kn2row_is_memory_lean():
+    """kn2row's defining property (§II.B(b): it transforms the kernel "in order to
+    decrease memory usage"): its workspace is the fp32 output accumulator, O(N*K*P*Q), below
+    im2col's R*S-fold copy of the input -- and nothing for fp32 NHWC outputs (accumulated in
+    place).  VGG conv3_2 at the bench batch (64 x 256 x 56 x 56, bf16)."""
+    import ctypes
+    lib = _lib.load()
+
+    def ws(algo, dtype, layout):
+        p = _lib.params(256, (3, 3), (1, 1), (1, 1), (1, 1), 1, True)
+        n = ctypes.c_size_t()
+        st = lib.ai3_conv2d_workspace_size(ctypes.byref(p), _lib.shape4((64, 256, 56, 56)), dtype, 0,
+                                           ai3.algo_id(algo), layout, layout, ctypes.byref(n))
+        assert st == _lib.OK
+        return n.value
+
+    out_f32 = 64 * 256 * 56 * 56 * 4
+    kn, gemm = ws("kn2row", _lib.BF16, _lib.NHWC), ws("gemm", _lib.BF16, _lib.NHWC)
+    assert kn < gemm / 4
+    assert kn <= out_f32 + (2 << 20)  # + the packed weights (1.2 MB)
+    # fp32 NHWC accumulates in place: nothing beyond what implicit_gemm needs (weights + the
+    # operand-rounding pass of the input)
+    assert ws("kn2row", _lib.F32, _lib.NHWC) <= ws("implicit_gemm", _lib.F32, _lib.NHWC)
