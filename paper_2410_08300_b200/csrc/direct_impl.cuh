@@ -1,0 +1,206 @@
+// direct_impl.cuh -- the `direct` algorithm (§II.B(d): "kernels are applied
+// directly to the input without transforming the data").
+//
+// CUDA-core FFMA with fp32 accumulation; bound by the FP32 pipe (VGG/ResNet
+// layers have >= 16 flop/byte against an 11.5 flop/byte FFMA ridge).
+//
+// One CTA (256 threads, 8 warps) computes 64 output channels x 256 output pixels (or 32 x
+// 512 for groups of <= 32 channels; 4 x 64 / 8 x 32 / 16 x 16 ... rows x columns, whichever
+// pads the layer's P x Q least) of one image / group.  Per chunk of CB input channels the CTA stages the
+// zero-padded input footprint and the chunk's weights ([cc][r][s][32 k], k fastest) in
+// shared memory.  Each thread owns an 8-channel x 8-pixel register tile (one output row,
+// 8 consecutive columns; 64 fp32 accumulators).  Per (channel, filter row) it reads its
+// input row segment once -- 128-bit loads for stride 1 -- and slides it across the S
+// filter columns in registers; the 8 weights of a tap are two broadcast 128-bit loads
+// (every lane of a warp shares its k group).  That is 64 FFMA per 2 weight loads plus
+// (8 + S - 1)/4 input loads: the FP32 pipe, not shared memory, is the limit.
+// Handles any stride / padding / dilation / groups and NCHW or NHWC, fp32 or bf16.
+#pragma once
+// (kernel template and per-tile-shape launcher; instantiated in direct_q2/q4/q8.cu so that
+// the 48 heavily unrolled variants compile in parallel; dispatch in direct.cu)
+#include <cstdlib>
+#include <cuda_bf16.h>
+#include "internal.h"
+#include "stage.cuh"
+
+namespace ai3 {
+
+namespace direct_detail {
+constexpr int NT = 256, VQ = 8;
+
+__device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
+    return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
+}
+}  // namespace direct_detail
+using namespace direct_detail;
+
+// KS: compile-time square kernel size (0 = runtime R, S).  UNIT: stride 1 and dilation 1
+// along w (the row segment is loaded with 128-bit loads and slid in registers).
+// NKG: k groups of 8 output channels per CTA (TK = 8 * NKG; 8 = one warp per k group, so
+// every staged input element feeds 64 channels).  QG: column groups of 8 pixels per tile
+// row; the tile is (256 / NKG / QG) rows x 8*QG columns, picked per layer so that small
+// feature maps (28x28, 14x14) do not pad to 64-wide tiles.
+template <int KS, bool UNIT, int QG, int NKG>
+__global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
+                                                            int xs_floats) {
+    constexpr int TK = 8 * NKG, PT = NT / NKG;  // pixel threads per k group
+    constexpr int TQ = VQ * QG, TP = PT / QG;
+    extern __shared__ __align__(16) float smem[];
+    const int R = KS ? KS : a.R;
+    const int S = KS ? KS : a.S;
+    const int tid = threadIdx.x;
+    const int qg = tid % QG, pr = (tid % PT) / QG, kg = tid / PT;  // a warp: one k group (broadcast weights)
+    const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
+    const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
+    const int k0g = blockIdx.y * TK;
+    const int n = blockIdx.z / a.G, g = blockIdx.z % a.G;
+    const int ih0 = p0 * a.sh - a.ph, iw0 = q0 * a.sw - a.pw;
+
+    float* xs = smem;              // [CB][FH][FWp]
+    float* ws = smem + xs_floats;  // [CB][R][S][TK]
+
+    float acc[8][VQ];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int i = 0; i < VQ; ++i) acc[j][i] = 0.f;
+
+    const int64_t xsN = a.in_nhwc ? a.H * a.W * a.C : a.C * a.H * a.W;
+    const int64_t xsC = a.in_nhwc ? 1 : a.H * a.W;
+    const int64_t xsH = a.in_nhwc ? a.W * a.C : a.W;
+    const int64_t xsW = a.in_nhwc ? a.C : 1;
+    const int64_t xbase = (int64_t)n * xsN + (int64_t)g * a.Cg * xsC;
+
+    for (int c0 = 0; c0 < a.Cg; c0 += CB) {
+        const int cb = min(CB, a.Cg - c0);
+        // ---- stage the input footprint (zeros outside the image)
+        // ---- weights [cc][r][s][TK]: contiguous 16-byte pieces of the prepared rows, copied
+        //      asynchronously (cp.async) so they stream in while the footprint is staged
+        {
+            const int nq = cb * R * S * (TK / 4);
+            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+            for (int i = tid; i < nq; i += NT) {
+                const int row = i / (TK / 4), qd = i % (TK / 4);  // row (cc, r, s), 4-channel piece
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + row * TK + 4 * qd);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
+                            ih0, iw0, cb, FH, FW, FWp, tid);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (int cc = 0; cc < cb; ++cc) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                const float* xrow = xs + (cc * FH + pr * a.sh + rr * a.dh) * FWp + qg * VQ * a.sw;
+                const float* wrow = ws + ((cc * R + rr) * S) * TK + kg * 8;
+                if (UNIT && KS) {
+                    // row segment xrow[0 .. VQ + S - 2] read once (16-byte aligned: FWp % 4 == 0,
+                    // qg * VQ % 4 == 0) and slid across the S filter columns in registers
+                    constexpr int NSEG = (VQ + (KS ? KS : 1) - 1 + 3) / 4;
+                    float xr[NSEG * 4];
+#pragma unroll
+                    for (int v = 0; v < NSEG; ++v) {
+                        const float4 t = *reinterpret_cast<const float4*>(xrow + 4 * v);
+                        xr[4 * v] = t.x; xr[4 * v + 1] = t.y; xr[4 * v + 2] = t.z; xr[4 * v + 3] = t.w;
+                    }
+#pragma unroll
+                    for (int ss = 0; ss < S; ++ss) {
+                        const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
+                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int i = 0; i < VQ; ++i) acc[j][i] = fmaf(wv[j], xr[i + ss], acc[j][i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int ss = 0; ss < S; ++ss) {
+                        const float4 w0 = *reinterpret_cast<const float4*>(wrow + ss * TK);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wrow + ss * TK + 4);
+                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                        float xv[VQ];
+#pragma unroll
+                        for (int i = 0; i < VQ; ++i) xv[i] = xrow[i * a.sw + ss * a.dw];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+#pragma unroll
+                            for (int i = 0; i < VQ; ++i) acc[j][i] = fmaf(wv[j], xv[i], acc[j][i]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: bias once at the end, optional ReLU, cast, store
+    const int p = p0 + pr;
+    if (p >= a.P) return;
+    const int qb = q0 + qg * VQ;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int kk = k0g + kg * 8 + j;
+        if (kk >= a.Kg) break;
+        const int64_t k = (int64_t)g * a.Kg + kk;
+        const float bv = a.bias ? a.bias[k] : 0.f;
+#pragma unroll
+        for (int i = 0; i < VQ; ++i) {
+            const int q = qb + i;
+            if (q >= a.Q) break;
+            float v = acc[j][i] + bv;
+            if (a.relu && v < 0.f) v = 0.f;
+            const int64_t o = a.out_nhwc ? (((int64_t)n * a.P + p) * a.Q + q) * a.K + k
+                                         : (((int64_t)n * a.K + k) * a.P + p) * a.Q + q;
+            if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[o] = __float2bfloat16_rn(v);
+            else reinterpret_cast<float*>(a.y)[o] = v;
+        }
+    }
+}
+
+template <int QG, int NKG>
+cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
+    constexpr int TK = 8 * NKG, TQ = VQ * QG, TP = NT / NKG / QG;
+    const bool unit = a.sw == 1 && a.dw == 1;
+    const int FH = (TP - 1) * a.sh + (a.R - 1) * a.dh + 1;
+    const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
+    // 16-byte aligned rows; unit-stride row segments read up to 3 floats past FW (never used)
+    int FWp = (FW + 3 + 3) / 4 * 4;
+    if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
+    const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
+    static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (dev knob AI3_DIRECT_KB)
+        const int kb = knob("AI3_DIRECT_KB", 48);
+        return (kb >= 8 && kb <= 100 ? kb : 48) * 1024;
+    }();
+    int CB = budget / per_c;
+    if (CB < 1) CB = 1;
+    if (CB > a.Cg) CB = a.Cg;
+    const int xs_floats = (CB * FH * FWp + 3) / 4 * 4;
+    const size_t smem = (size_t)xs_floats * 4 + (size_t)CB * a.R * a.S * TK * 4;
+    if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+    const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
+    dim3 grid(tiles, (unsigned)((a.Kg + TK - 1) / TK), (unsigned)(a.N * a.G));
+    if (grid.z > 65535) return cudaErrorInvalidConfiguration;
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp, xs_floats);
+    };
+    const bool sq = a.R == a.S;
+    if (unit) {
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG>);
+        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG, NKG>);
+        else launch(direct_conv_kernel<0, true, QG, NKG>);
+    } else {
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG, NKG>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG, NKG>);
+        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG, NKG>);
+        else launch(direct_conv_kernel<0, false, QG, NKG>);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ai3

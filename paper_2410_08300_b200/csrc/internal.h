@@ -26,6 +26,14 @@ struct StreamDeviceGuard {
     int prev = -1;
     explicit StreamDeviceGuard(void* stream) {
         if (!stream) return;
+        // under stream capture (CUDA graphs) the stream's device is the current one, and device
+        // queries other than the capture status would invalidate a global-mode capture
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(stream), &cs) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return;
+        }
+        if (cs != cudaStreamCaptureStatusNone) return;
         int sd = -1, cur = -1;
         if (cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), &sd) != cudaSuccess) {
             (void)cudaGetLastError();  // not a stream handle cudart knows: leave the device alone

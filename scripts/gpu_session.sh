@@ -6,7 +6,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo "build failed"; tail -20 gpurun_out/build.log; exit 1; }
 if [ "${TESTS:-1}" = "1" ]; then
-  timeout ${T_TESTS:-1500} python -m pytest tests -m gpu -q -x --timeout 600 --timeout-method thread -rfs --durations=30 \
+  timeout ${T_TESTS:-1500} python -m pytest tests -m gpu -q ${XFLAG} --timeout 600 --timeout-method thread -rfs --durations=30 \
       ${PYTEST_ARGS} > gpurun_out/pytest_gpu_full.txt 2>&1
   echo "pytest rc=$?"
   tail -45 gpurun_out/pytest_gpu_full.txt
