@@ -500,14 +500,17 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
         pl.ws_Vlo = ws;
         if (pl.splits == 2) ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
+        // M in bf16 for bf16 runs (halves the dominant M write + read: the transformed-domain
+        // products are rounded once more, R26), fp32 otherwise
+        const size_t m_elem = pl.cm == CM_BF16 ? 2 : 4;
         pl.ws_M = ws;
-        ws = align_up(ws + (size_t)16 * T * c.K * 4);
+        ws = align_up(ws + (size_t)16 * T * c.K * m_elem);
         a.a_mode = TC_A_TILED3D;
         a.M = (int)T;
         a.batch = 16;
         a.row_bytes = tiled_row_bytes(pl.Cpad * pl.elem);
         a.num_kb = (int)((pl.Cpad * pl.elem + a.row_bytes - 1) / a.row_bytes);
-        a.out_bf16 = 0;        // M is fp32
+        a.out_bf16 = pl.cm == CM_BF16 ? 1 : 0;  // M's element type
         a.epi_PQ = (int)T;     // [16][K][T] when the final output is NCHW
         a.out_bstride = (long long)T * c.K;
         pl.launches = (pl.need_prep ? 1 : 0) + 3;
@@ -832,8 +835,8 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
     if (pl.algo == AI3_ALGO_WINOGRAD) {
-        e = launch_winograd_output(reinterpret_cast<const float*>(w + pl.ws_M), tp.args.out_nchw, bias, y,
-                                   c.out_layout == AI3_NHWC, c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);
+        e = launch_winograd_output(w + pl.ws_M, tp.args.out_bf16, tp.args.out_nchw, bias, y, c.out_layout == AI3_NHWC,
+                                   c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);
         if (e != cudaSuccess) return cuda_fail(e, "winograd output transform launch");
     }
     return ok();

@@ -144,8 +144,8 @@ cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, 
 cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P,
                                   int64_t Q, int ph, int pw, ComputeMode cm, const void* x_lo, void* V, void* V_lo,
                                   cudaStream_t st);
-// M (fp32, [16][K][T] if out NCHW else [16][T][K]) -> y (+bias), cropped to P x Q.
-cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
+// M (fp32, or bf16 if m_bf16; [16][K][T] if out NCHW else [16][T][K]) -> y (+bias), cropped to P x Q.
+cudaError_t launch_winograd_output(const void* M, int m_bf16, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
                                    int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st);
 
 // ---------------------------------------------------------------- tcgen05 engine (tc_engine.cu)

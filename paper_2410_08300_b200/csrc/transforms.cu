@@ -456,7 +456,14 @@ __device__ __forceinline__ void wino_out4(const float (&m)[4][4], float bv, int 
     }
 }
 
-__global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, const float* __restrict__ bias, void* y,
+template <typename MT>
+__device__ __forceinline__ float ldm(const MT* p, int64_t i) {
+    if constexpr (sizeof(MT) == 2) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+    else return reinterpret_cast<const float*>(p)[i];
+}
+
+template <typename MT>
+__global__ void winograd_output_kernel(const MT* __restrict__ M, int m_kt, const float* __restrict__ bias, void* y,
                                        int out_nhwc, int bf16, int64_t N, int64_t K, int64_t P, int64_t Q,
                                        int64_t TH, int64_t TW, int relu) {
     const int64_t T = N * TH * TW;
@@ -470,7 +477,7 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) m[a][b] = M[(a * 4 + b) * plane + off];
+            for (int b = 0; b < 4; ++b) m[a][b] = ldm(M, (a * 4 + b) * plane + off);
         float yv[2][2];
         wino_out4(m, bias ? bias[k] : 0.f, relu, yv);
         const int64_t n = t / (TH * TW), th = (t / TW) % TH, tw = t % TW;
@@ -490,29 +497,49 @@ __global__ void winograd_output_kernel(const float* __restrict__ M, int m_kt, co
     }
 }
 
-// NHWC output, K % 4 == 0: one thread per (tile, 4 output channels).
-template <typename IDX>
-__global__ void __launch_bounds__(256) winograd_output_nhwc4_kernel(const float* __restrict__ M,
-                                                                    const float* __restrict__ bias, void* y, int bf16,
-                                                                    int64_t N, int64_t K, int64_t P, int64_t Q,
-                                                                    int64_t TH, int64_t TW, int relu) {
+// NHWC output, K % 8 == 0 (bf16 M) / K % 4 == 0 (fp32 M): one thread per (tile, VK output
+// channels): 16-byte M loads of all 16 components, one 16- (bf16 y, VK = 8) or 16-byte
+// (fp32 y, VK = 4) store per output pixel.
+template <typename IDX, typename MT, int VK>
+__global__ void __launch_bounds__(256) winograd_output_nhwc_kernel(const MT* __restrict__ M,
+                                                                   const float* __restrict__ bias, void* y, int bf16,
+                                                                   int64_t N, int64_t K, int64_t P, int64_t Q,
+                                                                   int64_t TH, int64_t TW, int relu) {
     const int64_t T = N * TH * TW;
-    const IDX kg = (IDX)(K / 4);
+    const IDX kg = (IDX)(K / VK);
     const IDX total = (IDX)(T * (int64_t)kg);
     const int64_t plane = T * K;
     for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
         const IDX ti = i / kg;
-        const int64_t t = ti, k0 = (int64_t)(i - ti * kg) * 4;
+        const int64_t t = ti, k0 = (int64_t)(i - ti * kg) * VK;
         const int64_t off = t * K + k0;
-        float4 mv[16];
+        float mv[16][VK];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) mv[j] = *reinterpret_cast<const float4*>(M + j * plane + off);
-        float out[4][2][2];
+        for (int j = 0; j < 16; ++j) {
+            if constexpr (sizeof(MT) == 2) {
+                static_assert(VK == 8, "bf16 M: 8 channels per 16-byte load");
+                const uint4 raw = *reinterpret_cast<const uint4*>(M + j * plane + off);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
+                for (int v = 0; v < 4; ++v) {
+                    const float2 f2 = __bfloat1622float2(h[v]);
+                    mv[j][2 * v] = f2.x;
+                    mv[j][2 * v + 1] = f2.y;
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < VK; v += 4) {
+                    const float4 f4 = *reinterpret_cast<const float4*>(M + j * plane + off + v);
+                    mv[j][v] = f4.x; mv[j][v + 1] = f4.y; mv[j][v + 2] = f4.z; mv[j][v + 3] = f4.w;
+                }
+            }
+        }
+        float out[VK][2][2];
+#pragma unroll
+        for (int v = 0; v < VK; ++v) {
             float m[4][4];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) m[j / 4][j % 4] = v == 0 ? mv[j].x : (v == 1 ? mv[j].y : (v == 2 ? mv[j].z : mv[j].w));
+            for (int j = 0; j < 16; ++j) m[j / 4][j % 4] = mv[j][v];
             wino_out4(m, bias ? bias[k0 + v] : 0.f, relu, out[v]);
         }
         const IDX thw = (IDX)(TH * TW), twi = (IDX)TW;
@@ -528,35 +555,56 @@ __global__ void __launch_bounds__(256) winograd_output_nhwc4_kernel(const float*
                 if (q >= Q) break;
                 const int64_t o = ((n * P + p) * Q + q) * K + k0;
                 if (bf16) {
-                    __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(out[0][a][b], out[1][a][b]),
-                                                        __floats2bfloat162_rn(out[2][a][b], out[3][a][b])};
-                    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + o) = *reinterpret_cast<const uint2*>(h);
+                    __align__(16) __nv_bfloat162 h[VK / 2];
+#pragma unroll
+                    for (int v = 0; v < VK / 2; ++v) h[v] = __floats2bfloat162_rn(out[2 * v][a][b], out[2 * v + 1][a][b]);
+                    if constexpr (VK == 8) {
+                        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(y) + o) = *reinterpret_cast<const uint4*>(h);
+                    } else {
+                        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + o) = *reinterpret_cast<const uint2*>(h);
+                    }
                 } else {
-                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + o) =
-                        make_float4(out[0][a][b], out[1][a][b], out[2][a][b], out[3][a][b]);
+#pragma unroll
+                    for (int v = 0; v < VK; v += 4)
+                        *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + o + v) =
+                            make_float4(out[v][a][b], out[v + 1][a][b], out[v + 2][a][b], out[v + 3][a][b]);
                 }
             }
         }
     }
 }
 
-cudaError_t launch_winograd_output(const float* M, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
-                                   int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st) {
+template <typename MT, int VK>
+static cudaError_t launch_wino_out_nhwc(const MT* M, const float* bias, void* y, int bf16, int64_t N, int64_t K,
+                                        int64_t P, int64_t Q, int64_t TH, int64_t TW, int relu, cudaStream_t st) {
+    const int64_t total = N * TH * TW * (K / VK);
+    const int64_t blocks = (total + 255) / 256;
+    const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+    if (total < (1LL << 31))
+        winograd_output_nhwc_kernel<uint32_t, MT, VK><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
+    else
+        winograd_output_nhwc_kernel<int64_t, MT, VK><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_winograd_output(const void* M, int m_bf16, int m_kt, const float* bias, void* y, int out_nhwc,
+                                   int bf16, int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st) {
     const int64_t TH = (P + 1) / 2, TW = (Q + 1) / 2;
-    if (!m_kt && out_nhwc && K % 4 == 0) {
-        const int64_t total = N * TH * TW * (K / 4);
-        const int64_t blocks = (total + 255) / 256;
-        const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-        if (total < (1LL << 31))
-            winograd_output_nhwc4_kernel<uint32_t><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
-        else
-            winograd_output_nhwc4_kernel<int64_t><<<grid, 256, 0, st>>>(M, bias, y, bf16, N, K, P, Q, TH, TW, relu);
-        return cudaGetLastError();
-    }
+    if (!m_kt && out_nhwc && m_bf16 && K % 8 == 0)
+        return launch_wino_out_nhwc<__nv_bfloat16, 8>(reinterpret_cast<const __nv_bfloat16*>(M), bias, y, bf16, N, K, P,
+                                                      Q, TH, TW, relu, st);
+    if (!m_kt && out_nhwc && !m_bf16 && K % 4 == 0)
+        return launch_wino_out_nhwc<float, 4>(reinterpret_cast<const float*>(M), bias, y, bf16, N, K, P, Q, TH, TW,
+                                              relu, st);
     const int64_t total = N * TH * TW * K;
     const int64_t blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
-    winograd_output_kernel<<<grid, 256, 0, st>>>(M, m_kt, bias, y, out_nhwc, bf16, N, K, P, Q, TH, TW, relu);
+    if (m_bf16)
+        winograd_output_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(M), m_kt,
+                                                                     bias, y, out_nhwc, bf16, N, K, P, Q, TH, TW, relu);
+    else
+        winograd_output_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(M), m_kt, bias, y, out_nhwc,
+                                                             bf16, N, K, P, Q, TH, TW, relu);
     return cudaGetLastError();
 }
 

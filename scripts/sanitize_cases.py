@@ -35,8 +35,11 @@ for s in SHAPES:
             if a == "winograd" and not (s.R == 3 and s.stride == 1):
                 continue
             for m in (("strict", "tf32") if dt == "f32" and a not in ("direct", "smm") else ("strict",)):
-                y = ai3.conv2d(xt, torch.from_numpy(w).cuda().to(tdt), torch.from_numpy(b).cuda().to(tdt), s.stride,
-                               s.pad, s.dil, s.groups, algorithm=a, math=m)
+                y = torch.full((s.N, s.K, s.P, s.Q), float("nan"), dtype=tdt, device="cuda")
+                if dt == "bf16":
+                    y = y.contiguous(memory_format=torch.channels_last)
+                ai3.conv2d(xt, torch.from_numpy(w).cuda().to(tdt), torch.from_numpy(b).cuda().to(tdt), s.stride,
+                           s.pad, s.dil, s.groups, algorithm=a, math=m, out=y)
                 torch.cuda.synchronize()
                 e = oracle.rel_err(y.double().cpu().numpy(), ref)
                 tol = 2e-2 if dt == "bf16" else (1e-5 if m == "strict" and a != "winograd" else 1e-3)

@@ -43,12 +43,17 @@ def run_ai3(shape: ConvShape, x, w, b, algo: str, dtype: str, math: str = "stric
     xt = to_device(x, dtype, layout)
     wt = to_device(w, dtype)
     bt = None if b is None else to_device(b, dtype)
+    # the output starts as NaN: an element a kernel fails to write fails the comparison
+    # instead of passing on a stale value of an earlier run that reused the same memory
+    fmt = torch.channels_last if layout == "nhwc" else torch.contiguous_format
+    y = torch.full((shape.N, shape.K, shape.P, shape.Q), float("nan"), dtype=xt.dtype, device=xt.device) \
+        .contiguous(memory_format=fmt)
     if plan:
         p = ai3.ConvPlan(wt, bt, xt.shape, shape.stride, shape.pad, shape.dil, shape.groups, algo, math,
                          in_layout=1 if layout == "nhwc" else 0)
-        y = p(xt)
+        p(xt, out=y)
     else:
-        y = ai3.conv2d(xt, wt, bt, shape.stride, shape.pad, shape.dil, shape.groups, algo, math)
+        ai3.conv2d(xt, wt, bt, shape.stride, shape.pad, shape.dil, shape.groups, algo, math, out=y)
     torch.cuda.synchronize()
     return y.float().contiguous().cpu().numpy().astype(np.float64)
 

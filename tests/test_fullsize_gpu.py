@@ -106,8 +106,11 @@ def test_fullsize_parity(net, i, algo, dtype, math):
         ai3.autotune(x, wt, bt, spec.stride, spec.pad, spec.dil, spec.groups, math)
     plan = ai3.ConvPlan(wt, bt, x.shape, spec.stride, spec.pad, spec.dil, spec.groups, algo, math,
                         in_layout=1, out_layout=1)
-    y = plan(x)
+    y = torch.full(plan.out_shape, float("nan"), dtype=tdt, device=x.device).contiguous(
+        memory_format=torch.channels_last)  # unwritten outputs stay NaN and fail
+    plan(x, out=y)
     torch.cuda.synchronize()
+    assert not bool(torch.isnan(y).any()), "some output elements were never written"
     tol = 1e-3 if (algo == "winograd" or plan.algorithm == "winograd") and dtype == "f32" else TOL[(dtype, math)]
     got_full = y[imgs].double().cpu().numpy()
     ii = torch.from_numpy(idx).cuda()

@@ -49,6 +49,8 @@ bi[-1] = 1.0  # the channel the mutant breaks carries a bias
 ri = oracle.conv2d(xi, wi, bi, 1, 1, 1, 1)
 xt = torch.from_numpy(xi.astype(np.float32)).cuda().bfloat16().contiguous(memory_format=torch.channels_last)
 for algo in json.loads(sys.argv[3]):
+    if algo == "winograd":
+        continue  # bf16 Winograd rounds M to bf16 (DESIGN.md R26): not bit-exact; the fp32 case covers it
     p = ai3.ConvPlan(torch.from_numpy(wi.astype(np.float32)).cuda().bfloat16(),
                      torch.from_numpy(bi.astype(np.float32)).cuda().bfloat16(), xt.shape, 1, 1, 1, 1, algo,
                      in_layout=1)
@@ -77,6 +79,8 @@ def test_mutant_library_fails_parity_and_product_passes():
     for algo in ALGOS:
         tol = 1e-3 if algo == "winograd" else 1e-5
         assert good["f32/" + algo] <= tol, (algo, good)
-        assert good["int/" + algo] == 0.0, (algo, good)
+        if algo != "winograd":
+            assert good["int/" + algo] == 0.0, (algo, good)
         assert bad["f32/" + algo] > tol, f"mutant not caught by the fp32 harness on {algo}: {bad}"
-        assert bad["int/" + algo] > 0.0, f"mutant not caught by the bit-exact harness on {algo}: {bad}"
+        if algo != "winograd":
+            assert bad["int/" + algo] > 0.0, f"mutant not caught by the bit-exact harness on {algo}: {bad}"

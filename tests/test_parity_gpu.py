@@ -136,6 +136,11 @@ def test_integer_inputs_bit_exact(shape, algo, dtype, math):
     y = run_ai3(shape, x, w, b, algo, dtype, math, "nhwc")
     r = ref(shape, x, w, b)
     assert np.abs(r).max() < (256 if small else 2 ** 24)
+    if algo == "winograd" and dtype == "bf16":
+        # bf16 Winograd stores the transformed-domain products M in bf16 (R26): the
+        # one inexact step; the result stays within the bf16 bound
+        assert oracle.rel_err(y, r) <= 2e-2
+        return
     np.testing.assert_array_equal(y, r)
 
 
