@@ -45,9 +45,8 @@ def _run(x, w, b, stride, pad, dtype, math, layout, algo="implicit_gemm"):
     xt = to_device(x, dtype, layout)
     wt = to_device(w, dtype)
     bt = None if b is None else to_device(b, dtype)
-    P = (x.shape[2] + 2 * pad - w.shape[2]) // stride + 1
-    Q = (x.shape[3] + 2 * pad - w.shape[3]) // stride + 1
-    y = torch.full((x.shape[0], w.shape[0], P, Q), float("nan"), dtype=xt.dtype, device=xt.device).contiguous(
+    oshape = ai3.output_shape(x.shape, w.shape[0], w.shape[2:], stride, pad)
+    y = torch.full(oshape, float("nan"), dtype=xt.dtype, device=xt.device).contiguous(
         memory_format=torch.channels_last if layout == "nhwc" else torch.contiguous_format)  # unwritten -> NaN
     ai3.conv2d(xt, wt, bt, stride, pad, 1, 1, algo, math, out=y)
     torch.cuda.synchronize()
