@@ -524,7 +524,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
     {
         const bool allow = knob("AI3_BOX64", 1) != 0;
-        if (allow && a.stg_row == 64 && a.out_bf16 && a.block_n % 64 == 0 && a.batch == 1) {
+        if (allow && a.stg_row == 64 && a.out_bf16 && a.block_n % 64 == 0) {
             a.box64 = 1;
             a.stg_row = 128;
             tc_configure(pl.tc, device_num_sms());  // re-derive stages / staging with 4 KB buffers
@@ -675,8 +675,8 @@ ai3_status encode_out_map(ai3_plan& pl, void* out) {
     } else if (a.batch > 1) {
         const uint64_t dims[3] = {(uint64_t)a.Ncols, (uint64_t)a.M, (uint64_t)a.batch};
         const uint64_t str[2] = {(uint64_t)a.Ncols * eo, (uint64_t)a.out_bstride * eo};
-        const uint32_t box[3] = {32, 32, 1};
-        okm = encode_tiled(&pl.tout, dt, 3, out, dims, str, box, sw);
+        const uint32_t box[3] = {a.box64 ? 64u : 32u, 32, 1};
+        okm = encode_tiled(&pl.tout, dt, 3, out, dims, str, box, a.box64 ? CU_TENSOR_MAP_SWIZZLE_128B : sw);
     } else {
         const uint64_t dims[2] = {(uint64_t)a.Ncols, (uint64_t)a.M};
         const uint64_t str[1] = {(uint64_t)a.Ncols * eo};

@@ -778,7 +778,8 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
             n0 = 0;
             row0 = hp0 + quarter * (32 / a.TQ);
         } else {
-            const int rem = tile % tiles_per_batch;
+            img = tile / tiles_per_batch;  // batch index (Winograd's 16 GEMMs) for the 3-D store
+            const int rem = tile - img * tiles_per_batch;
             const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
             n0 = ((rem % a.n_tiles) * a.n2 + sub) * a.block_n;
             row0 = m0 + quarter * 32;
@@ -860,6 +861,7 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                     const uint8_t* src = my_stg + slot * 32 * ROWB;
                     const int cx = col0 - 32 * half;
                     if (HALO) tma_store_4d(&tout, src, cx, qc, row0, img);
+                    else if (a.batch > 1) tma_store_3d(&tout, src, cx, row0, img);
                     else tma_store_2d(&tout, src, cx, row0);
                     bulk_commit_group();
                 }
@@ -985,7 +987,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             named_bar_sync(1, 32 * NUM_EPI_WARPS);
         }
         const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.stg_row != 0 &&
-                          (a.bias == nullptr || a.bias_smem) && !a.trace && a.batch == 1 &&
+                          (a.bias == nullptr || a.bias_smem) && !a.trace &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
         // invariant: N sub-tiles are configured for the fast epilogue only (tc_configure), and
         // execute() rejects outputs that would turn the TMA stores off for such a plan

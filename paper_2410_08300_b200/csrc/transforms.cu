@@ -513,34 +513,54 @@ __global__ void __launch_bounds__(256) winograd_output_nhwc_kernel(const MT* __r
         const IDX ti = i / kg;
         const int64_t t = ti, k0 = (int64_t)(i - ti * kg) * VK;
         const int64_t off = t * K + k0;
-        float mv[16][VK];
+        // A^T M accumulated one row xi of M at a time (4 components of VK channels live at once):
+        // at[0] = m0 + m1 + m2, at[1] = m1 - m2 - m3 (rows of A^T = [[1,1,1,0],[0,1,-1,-1]])
+        float at[2][4][VK];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if constexpr (sizeof(MT) == 2) {
-                static_assert(VK == 8, "bf16 M: 8 channels per 16-byte load");
-                const uint4 raw = *reinterpret_cast<const uint4*>(M + j * plane + off);
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        for (int xi = 0; xi < 4; ++xi) {
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const float2 f2 = __bfloat1622float2(h[v]);
-                    mv[j][2 * v] = f2.x;
-                    mv[j][2 * v + 1] = f2.y;
+            for (int nu = 0; nu < 4; ++nu) {
+                float mv[VK];
+                const int j = xi * 4 + nu;
+                if constexpr (sizeof(MT) == 2) {
+                    static_assert(VK == 8, "bf16 M: 8 channels per 16-byte load");
+                    const uint4 raw = *reinterpret_cast<const uint4*>(M + j * plane + off);
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const float2 f2 = __bfloat1622float2(h[v]);
+                        mv[2 * v] = f2.x;
+                        mv[2 * v + 1] = f2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VK; v += 4) {
+                        const float4 f4 = *reinterpret_cast<const float4*>(M + j * plane + off + v);
+                        mv[v] = f4.x; mv[v + 1] = f4.y; mv[v + 2] = f4.z; mv[v + 3] = f4.w;
+                    }
                 }
-            } else {
 #pragma unroll
-                for (int v = 0; v < VK; v += 4) {
-                    const float4 f4 = *reinterpret_cast<const float4*>(M + j * plane + off + v);
-                    mv[j][v] = f4.x; mv[j][v + 1] = f4.y; mv[j][v + 2] = f4.z; mv[j][v + 3] = f4.w;
+                for (int v = 0; v < VK; ++v) {
+                    if (xi == 0) { at[0][nu][v] = mv[v]; at[1][nu][v] = 0.f; }
+                    else if (xi == 1) { at[0][nu][v] += mv[v]; at[1][nu][v] += mv[v]; }
+                    else if (xi == 2) { at[0][nu][v] += mv[v]; at[1][nu][v] -= mv[v]; }
+                    else { at[1][nu][v] -= mv[v]; }
                 }
             }
         }
+        // (A^T M) A + bias (+ ReLU): out[v][a][b]
         float out[VK][2][2];
 #pragma unroll
         for (int v = 0; v < VK; ++v) {
-            float m[4][4];
+            const float bv = bias ? bias[k0 + v] : 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) m[j / 4][j % 4] = mv[j][v];
-            wino_out4(m, bias ? bias[k0 + v] : 0.f, relu, out[v]);
+            for (int r = 0; r < 2; ++r) {
+                float o0 = at[r][0][v] + at[r][1][v] + at[r][2][v] + bv;
+                float o1 = at[r][1][v] - at[r][2][v] - at[r][3][v] + bv;
+                if (relu) { o0 = o0 < 0.f ? 0.f : o0; o1 = o1 < 0.f ? 0.f : o1; }  // NaN passes (torch.relu)
+                out[v][r][0] = o0;
+                out[v][r][1] = o1;
+            }
         }
         const IDX thw = (IDX)(TH * TW), twi = (IDX)TW;
         const IDX ni = ti / thw, rem = ti - ni * thw;
