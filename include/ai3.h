@@ -233,6 +233,18 @@ void ai3_conv2d_plan_destroy(ai3_plan* plan);
  * Set before the plan's first use on a stream; 0 restores the plain convolution. */
 ai3_status ai3_conv2d_plan_set_relu(ai3_plan* plan, int32_t relu);
 
+/* Fused 2x2 / stride-2 max pooling (the conv -> ReLU -> pool
+ * chains of VGG are "completely managed by the framework"): after
+ * ai3_conv2d_plan_set_maxpool2x2(plan, 1) every execute writes y = max_pool2d(conv (+bias)
+ * (+ReLU), kernel 2, stride 2, padding 0, floor mode) -- shape (N, K, P/2, Q/2), the plan's
+ * layout -- and the full-resolution conv output never reaches memory.  Max pooling is taken
+ * in fp32 before the output cast (identical bits to pooling the cast values: rounding is
+ * monotonic); NaN propagates as in torch.  Returns AI3_ERR_UNSUPPORTED (plan unchanged)
+ * unless the plan is a bf16 NHWC implicit_gemm plan in a halo mode (the pooling windows
+ * then lie inside one warp's 4 x 8 output pixels) with P, Q >= 2; callers then pool with
+ * ai3_maxpool2d.  y must be 16-byte aligned.  0 restores the plain output. */
+ai3_status ai3_conv2d_plan_set_maxpool2x2(ai3_plan* plan, int32_t enable);
+
 /* ------------------------------------------------------------------ linear
  *
  * y[b][o] = bias[o] + sum_i x[b][i] * w[o][i]   (torch.nn.Linear; x [batch][in] row-major,

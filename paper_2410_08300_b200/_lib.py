@@ -36,7 +36,7 @@ EXPORTS = ["ai3_version", "ai3_last_error", "ai3_algo_name", "ai3_algo_from_name
            "ai3_conv2d_plan_set_relu", "ai3_linear_plan_weight_bytes", "ai3_linear_plan_create", "ai3_relu",
            "ai3_pool2d_output_shape", "ai3_maxpool2d", "ai3_avgpool2d", "ai3_adaptive_avgpool2d",
            "ai3_layout_copy", "ai3_conv2d_autotune_scratch_bytes", "ai3_conv2d_autotune",
-           "ai3_conv2d_autotune_clear", "ai3_conv2d_plans_execute_host"]
+           "ai3_conv2d_autotune_clear", "ai3_conv2d_plans_execute_host", "ai3_conv2d_plan_set_maxpool2x2"]
 
 
 class Ai3LibraryMissing(RuntimeError):
@@ -121,6 +121,7 @@ def load():
         "ai3_conv2d_custom": ([ctypes.c_char_p, ctypes.POINTER(Tensor4d), ctypes.POINTER(Tensor4d), vp, i32x2, i32x2,
                                i32x2, i32, ctypes.POINTER(Tensor4d), vp], ctypes.c_int),
         "ai3_conv2d_plan_set_relu": ([vp, i32], ctypes.c_int),
+        "ai3_conv2d_plan_set_maxpool2x2": ([vp, i32], ctypes.c_int),
         "ai3_linear_plan_weight_bytes": ([i64, i64, i64, i32, ctypes.c_int, ctypes.c_int, ctypes.POINTER(sz)],
                                          ctypes.c_int),
         "ai3_linear_plan_create": ([i64, i64, i64, ctypes.c_int, ctypes.c_int, vp, vp, vp, sz, vp,

@@ -319,6 +319,9 @@ class ConvPlan:
         self.out_layout = in_layout if out_layout is None else out_layout
         self.out_shape = output_shape(self.in_shape, weight.shape[0], weight.shape[2:], self.stride, self.padding,
                                       self.dilation, groups)
+        self.conv_shape = self.out_shape
+        self.relu = False
+        self.pool = False
         self._prm = _lib.params(weight.shape[0], weight.shape[2:], self.stride, self.padding, self.dilation, groups,
                                 bias is not None)
         aid = algo_id(algorithm)
@@ -365,6 +368,16 @@ class ConvPlan:
         """Fuse a ReLU into the plan's output epilogue (ai3_conv2d_plan_set_relu)."""
         _check(_lib.load().ai3_conv2d_plan_set_relu(self._h, 1 if relu else 0))
         self.relu = bool(relu)
+        return self
+
+    def set_maxpool2x2(self, pool: bool = True) -> "ConvPlan":
+        """Fuse a 2x2 / stride-2 max pooling into the epilogue (ai3_conv2d_plan_set_maxpool2x2):
+        the plan then outputs (N, K, P // 2, Q // 2).  Raises UnsupportedConfiguration (plan
+        unchanged) when the plan's kernel mode cannot pool in its epilogue."""
+        _check(_lib.load().ai3_conv2d_plan_set_maxpool2x2(self._h, 1 if pool else 0))
+        n, k, p, q = self.conv_shape
+        self.out_shape = (n, k, p // 2, q // 2) if pool else self.conv_shape
+        self.pool = bool(pool)
         return self
 
     def execute_raw(self, x_ptr: int, y_ptr: int, ws_ptr: int | None, ws_bytes: int, stream_ptr: int):

@@ -282,6 +282,8 @@ struct ai3_plan {
     CUtensorMap tout{};
     int launches = 1;
     int relu = 0;  // fused ReLU epilogue (ai3_conv2d_plan_set_relu)
+    int pool = 0;  // fused 2x2 / stride-2 max pooling (ai3_conv2d_plan_set_maxpool2x2): y is (N, K, P/2, Q/2)
+    int cached_out_pool = 0;
     bool kn_inplace = false;  // kn2row: fp32 NHWC output accumulates in y itself (no workspace)
     int kn_first = -1;        // kn2row: a tap covering every output pixel (runs first, writes), or -1
 };
@@ -660,17 +662,19 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
 // Encode (or reuse) the output tensor map of the TMA-store epilogue for destination `out`.
 ai3_status encode_out_map(ai3_plan& pl, void* out) {
     const TcArgs& a = pl.tc.args;
-    if (a.stg_row == 0 || pl.cached_out == out) return ok();
+    if (a.stg_row == 0 || (pl.cached_out == out && pl.cached_out_pool == pl.pool)) return ok();
     const int eo = a.out_bf16 ? 2 : 4;
     const CUtensorMapDataType dt = a.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const CUtensorMapSwizzle sw = a.stg_row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
     bool okm;
     const ConvProblem& c = pl.pb;
     if (a.a_mode == TC_A_HALO) {
-        const uint64_t dims[4] = {(uint64_t)a.Ncols, (uint64_t)c.Q, (uint64_t)c.P, (uint64_t)c.N};
-        const uint64_t str[3] = {(uint64_t)a.Ncols * eo, (uint64_t)c.Q * a.Ncols * eo,
-                                 (uint64_t)c.P * c.Q * a.Ncols * eo};
-        const uint32_t box[4] = {a.box64 ? 64u : 32u, (uint32_t)a.TQ, (uint32_t)(32 / a.TQ), 1};
+        // pooled: the (N, P/2, Q/2, K) output, each warp storing its 2 x 4 pooled pixels
+        const uint64_t Po = pl.pool ? (uint64_t)c.P / 2 : (uint64_t)c.P, Qo = pl.pool ? (uint64_t)c.Q / 2 : (uint64_t)c.Q;
+        const uint64_t dims[4] = {(uint64_t)a.Ncols, Qo, Po, (uint64_t)c.N};
+        const uint64_t str[3] = {(uint64_t)a.Ncols * eo, Qo * a.Ncols * eo, Po * Qo * a.Ncols * eo};
+        const uint32_t box[4] = {a.box64 ? 64u : 32u, (uint32_t)(pl.pool ? a.TQ / 2 : a.TQ),
+                                 (uint32_t)(pl.pool ? 16 / a.TQ : 32 / a.TQ), 1};
         okm = encode_tiled(&pl.tout, dt, 4, out, dims, str, box, a.box64 ? CU_TENSOR_MAP_SWIZZLE_128B : sw);
     } else if (a.batch > 1) {
         const uint64_t dims[3] = {(uint64_t)a.Ncols, (uint64_t)a.M, (uint64_t)a.batch};
@@ -688,6 +692,7 @@ ai3_status encode_out_map(ai3_plan& pl, void* out) {
         return fail(AI3_ERR_CUDA, "tensor-map encoding failed for the output (%s)", ai3_algo_name(pl.algo));
     }
     pl.cached_out = out;
+    pl.cached_out_pool = pl.pool;
     return ok();
 }
 
@@ -775,6 +780,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     TcPlan tp = pl.tc;
     tp.args.bias = bias;
     tp.args.relu = pl.relu;  // the GEMM's output is y (implicit_gemm, gemm); cleared below otherwise
+    tp.args.pool = pl.pool;
     ai3_status s;
     if (pl.algo == AI3_ALGO_IMPLICIT_GEMM || pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
@@ -825,7 +831,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.relu = 0;
     }
     if (tp.args.stg_row && !aligned(tp.args.out, 16)) {  // TMA stores need a 16-byte base
-        if (tp.args.n2 == 2)  // two N sub-tiles per unit run only with the TMA-store epilogue
+        if (tp.args.n2 == 2 || tp.args.pool)  // these run only with the TMA-store epilogue
             return fail(AI3_ERR_INVALID_ARGUMENT, "y must be 16-byte aligned for this plan (%s, %lld output channels)",
                         ai3_algo_name(pl.algo), (long long)c.K);
         tp.args.stg_row = 0;
@@ -853,6 +859,13 @@ ai3_status check_tensor(const ai3_tensor4d* t, const char* what) {
 size_t act_bytes(const ConvProblem& c, bool output) {
     const size_t e = c.dtype == AI3_BF16 ? 2 : 4;
     return output ? (size_t)(c.N * c.K * c.P * c.Q) * e : (size_t)(c.N * c.C * c.H * c.W) * e;
+}
+
+// bytes of a plan's output tensor (the pooled one when 2x2 max pooling is fused)
+size_t out_bytes(const ai3_plan& pl) {
+    const ConvProblem& c = pl.outer;
+    const size_t e = c.dtype == AI3_BF16 ? 2 : 4;
+    return pl.pool ? (size_t)(c.N * c.K * (c.P / 2) * (c.Q / 2)) * e : act_bytes(c, true);
 }
 
 }  // namespace
@@ -1018,7 +1031,7 @@ ai3_status ai3_conv2d_plan_execute_host(ai3_plan* plan, const void* x_host, void
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
     ai3_status s = execute(*plan, x_dev, y_dev, workspace, workspace_bytes, st);
     if (s != AI3_OK) return s;
-    e = cudaMemcpyAsync(y_host, y_dev, act_bytes(plan->outer, true), cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(y_host, y_dev, out_bytes(*plan), cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy of y");
     return ok();
 }
@@ -1069,7 +1082,7 @@ ai3_status ai3_conv2d_plans_execute_host(int32_t n, ai3_plan* const* plans, cons
         e = cudaEventRecord(ev[2 * i + 1], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev[2 * i + 1], 0);  // ...and leaves while i+1 computes
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(y_hosts[i], y_devs[i], act_bytes(plans[i]->outer, true), cudaMemcpyDeviceToHost, d2h);
+            e = cudaMemcpyAsync(y_hosts[i], y_devs[i], out_bytes(*plans[i]), cudaMemcpyDeviceToHost, d2h);
     }
     if (e == cudaSuccess) e = cudaEventRecord(done, d2h);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, done, 0);  // join: `stream` covers every copy
@@ -1109,6 +1122,29 @@ ai3_status ai3_linear_plan_create(int64_t batch, int64_t in_features, int64_t ou
     const int64_t in_shape[4] = {batch, in_features, 1, 1};
     return ai3_conv2d_plan_create(&p, in_shape, dtype, math, AI3_ALGO_IMPLICIT_GEMM, AI3_NHWC, AI3_NHWC, w, bias,
                                   weight_buf, weight_bytes, stream, out);
+}
+
+ai3_status ai3_conv2d_plan_set_maxpool2x2(ai3_plan* plan, int32_t enable) {
+    if (!plan) return fail(AI3_ERR_INVALID_ARGUMENT, "null plan");
+    std::lock_guard<std::mutex> lock(plan->mu);
+    if (!enable) {
+        plan->pool = 0;
+        return ok();
+    }
+    const TcArgs& a = plan->tc.args;
+    const ConvProblem& c = plan->pb;
+    // the pooling windows must be whole inside a warp's 4 x 8-pixel block of a halo tile, and the
+    // compile-time-specialised TMA-store epilogue must run (bf16 NHWC output, one accumulation chunk)
+    const bool ok_mode = plan->algo == AI3_ALGO_IMPLICIT_GEMM && a.a_mode == TC_A_HALO && a.TQ == 8 && a.TP % 2 == 0;
+    const bool ok_epi = plan->cm == CM_BF16 && a.out_bf16 && !a.out_nchw && a.stg_row != 0 && a.epi_fast && !a.trace &&
+                        (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && (!plan->bias_present || a.bias_smem);
+    if (!ok_mode || !ok_epi || c.P < 2 || c.Q < 2)
+        return fail(AI3_ERR_UNSUPPORTED,
+                    "fused 2x2 max pooling needs a bf16 NHWC implicit_gemm plan in a halo mode (stride-1 3x3-class "
+                    "conv, K <= 128 or 64-channel chunks) with P, Q >= 2 (this plan: %s, mode %d)",
+                    ai3_algo_name(plan->algo), a.a_mode);
+    plan->pool = 1;
+    return ok();
 }
 
 ai3_status ai3_conv2d_plan_set_relu(ai3_plan* plan, int32_t relu) {

@@ -190,6 +190,8 @@ struct TcArgs {
     int bias_smem;  // 1: the epilogue stages the fp32 bias in shared memory
     int box64;      // bf16 TMA-store rows of 64 channels (two 32-column chunks per store)
     int relu;       // 1: fused ReLU after the bias (model path)
+    int pool;       // 1: fused 2x2 / stride-2 max pooling of the tile (halo modes, fast epilogue; row f1):
+                    // `out` is the pooled NHWC tensor (N, P/2, Q/2, K)
     int pf_tiles;   // TILED2D: prefetch the A panel of the tile this many scheduler steps ahead into L2 (0 = off)
     // kn2row tap epilogue (a_mode TILED2D over the input pixels [N*H*W][Cpad], one launch per
     // filter tap): row m = input pixel (n, h, w) adds its K partial sums into the fp32 output

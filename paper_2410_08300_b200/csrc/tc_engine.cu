@@ -735,6 +735,9 @@ __device__ __forceinline__ void mma_issuer_halo_chunked(const TcArgs& a, uint8_t
     }
 }
 
+// torch.max semantics: NaN propagates (max_pool2d of a NaN window is NaN)
+__device__ __forceinline__ float nan_max(float a, float b) { return (a != a || a > b) ? a : b; }
+
 // ---------------------------------------------------------------- fast epilogue
 // The common case -- bf16 NHWC output through TMA stores, bias (if any) staged in smem,
 // one accumulation chunk per tile -- with every configuration choice resolved at compile
@@ -836,6 +839,18 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
                 }
+                // fused 2x2 / stride-2 max pooling (row f1): in halo tiles TMEM lane = p_l * 8 + q_l,
+                // so a pooling window is lanes {l, l^1, l^8, l^9}; lanes with (l & 9) == 0 keep the
+                // window's max.  bf16 rounding is monotonic, so pooling before the cast is
+                // bit-identical to casting first and pooling after (the unfused model path).
+                const bool pooled = HALO && a.pool;
+                if (pooled) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        f[j] = nan_max(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+                        f[j] = nan_max(f[j], __shfl_xor_sync(0xffffffffu, f[j], 8));
+                    }
+                }
                 const int half = BOX64 ? hh : 0;
                 const uint32_t buf = stg_u32 + slot * 32 * ROWB;
                 if (half == 0 && issued >= n_stg) {  // slot reuse: that store must have read smem
@@ -846,12 +861,27 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                     }
                     __syncwarp();
                 }
+                if (!pooled) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    __nv_bfloat162 h[4];
+                    for (int q = 0; q < 4; ++q) {
+                        __nv_bfloat162 h[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
-                    sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(h));
+                        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+                        sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(h));
+                    }
+                } else if ((lane & 9) == 0) {
+                    // pooled pixel (p_l / 2, q_l / 2) of this warp's 2 x 4 block -> staged row pr
+                    const int pr = ((lane >> 4) << 2) | ((lane & 7) >> 1);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        __nv_bfloat162 h[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
+                        const int qq = q + 4 * half;
+                        const uint32_t off = BOX64 ? (uint32_t)(pr * 128 + ((qq ^ (pr & 7)) << 4))
+                                                   : (uint32_t)(pr * 64 + ((qq ^ ((pr >> 1) & 3)) << 4));
+                        sts128(buf + off, *reinterpret_cast<uint4*>(h));
+                    }
                 }
                 const bool last = col0 + 32 >= a.Ncols;
                 if (BOX64 && half == 0 && !last) continue;
@@ -860,7 +890,8 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 if (lane == 0) {
                     const uint8_t* src = my_stg + slot * 32 * ROWB;
                     const int cx = col0 - 32 * half;
-                    if (HALO) tma_store_4d(&tout, src, cx, qc, row0, img);
+                    if (pooled) tma_store_4d(&tout, src, cx, qc >> 1, row0 >> 1, img);
+                    else if (HALO) tma_store_4d(&tout, src, cx, qc, row0, img);
                     else if (a.batch > 1) tma_store_3d(&tout, src, cx, row0, img);
                     else tma_store_2d(&tout, src, cx, row0);
                     bulk_commit_group();
@@ -991,7 +1022,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
         // invariant: N sub-tiles are configured for the fast epilogue only (tc_configure), and
         // execute() rejects outputs that would turn the TMA stores off for such a plan
-        if (a.n2 == 2 && !fast) __trap();
+        if ((a.n2 == 2 || a.pool) && !fast) __trap();
         if (fast) {
             const uint32_t sb = smem_u32(sbias);
             if (a.a_mode == TC_A_HALO) {

@@ -93,6 +93,7 @@ class Conv2D(nn.Module):
         self.math = math
         self.layer_name = name
         self.relu = False  # fused ReLU epilogue (set by swap_backend for conv -> relu pairs)
+        self.pool = False  # fused 2x2 / stride-2 max pooling (set by swap_backend for conv (-> relu) -> pool)
         self._plans = {}
 
     def extra_repr(self):
@@ -112,6 +113,12 @@ class Conv2D(nn.Module):
                             self.algorithm, self.math, in_layout=lay, dtype=x.dtype)
             if self.relu:
                 plan.set_relu(True)
+            plan.pool_fallback = False
+            if self.pool:
+                try:
+                    plan.set_maxpool2x2(True)
+                except UnsupportedConfiguration:  # this plan's kernel mode cannot pool: separate ai3 pass
+                    plan.pool_fallback = True
             ent = (wv, plan)
             self._plans[key] = ent
         return ent[1]
@@ -127,8 +134,16 @@ class Conv2D(nn.Module):
             if self.relu:
                 from .layers import relu
                 y = relu(y, inplace=True)
+            if self.pool:
+                from .layers import max_pool2d
+                y = max_pool2d(y, 2, 2)
             return y
-        return self.plan_for(x)(x)
+        plan = self.plan_for(x)
+        y = plan(x)
+        if plan.pool_fallback:
+            from .layers import max_pool2d
+            y = max_pool2d(y, 2, 2)
+        return y
 
 
 def _resolve(selector: Selector, module: nn.Conv2d, index: int) -> str:
@@ -359,6 +374,38 @@ def swap_backend(module: nn.Module, algos: Mapping[str, Selector] | None = None,
             node.replace_all_uses_with(src)
             graph.erase_node(node)
             replaced.append((src.name, "fused_relu"))
+
+    # fusion: conv2d (-> relu) -> max_pool2d(2, 2) (sole consumer, floor mode, no padding or
+    # dilation) runs as one kernel: the epilogue pools and the conv output never reaches memory
+    def _is_pool2x2(n):
+        m = _mod(n)
+        if isinstance(m, L.MaxPool2D):
+            k, st, pd, dl, ceil = m.args
+        elif n.op == "call_function" and n.target is L.max_pool2d:
+            names = ("kernel_size", "stride", "padding", "dilation", "ceil_mode")
+            vals = dict(zip(names, list(n.args[1:]))) | {k2: v for k2, v in n.kwargs.items() if k2 in names}
+            k, st, pd, dl, ceil = (vals.get("kernel_size"), vals.get("stride"), vals.get("padding", 0),
+                                   vals.get("dilation", 1), vals.get("ceil_mode", False))
+            if st is None:
+                st = k
+        else:
+            return False
+        two = lambda v: v in (2, (2, 2), [2, 2])  # noqa: E731
+        zero = lambda v: v in (0, (0, 0), [0, 0])  # noqa: E731
+        one = lambda v: v in (1, (1, 1), [1, 1])  # noqa: E731
+        return two(k) and two(st) and zero(pd) and one(dl) and not ceil
+
+    for node in list(graph.nodes):
+        if not _is_pool2x2(node) or not node.args or not isinstance(node.args[0], torch.fx.Node):
+            continue
+        src = node.args[0]
+        producer = _mod(src)
+        if isinstance(producer, Conv2D) and len(src.users) == 1 and not producer.pool and \
+                calls.get(src.target) == 1:
+            producer.pool = True
+            node.replace_all_uses_with(src)
+            graph.erase_node(node)
+            replaced.append((src.name, "fused_maxpool2x2"))
 
     # fusion: flatten(x, 1) -> linear is one convolution with an H x W kernel over x, which
     # reads the (NHWC) activation in place (layers.Linear.fused_flatten)

@@ -17,6 +17,7 @@ from torch import nn
 
 import oracle
 from oracle import ops as oops
+from synth import ConvShape, conv_inputs
 
 pytestmark = pytest.mark.gpu
 
@@ -253,3 +254,49 @@ def test_swap_backend_vgg16_all_ai3(dtype):
         y = _host(model(x))
     ref = _oracle_vgg16(vgg, _host(x))
     assert _rel(y, ref) <= (1e-4 if dtype == "f32" else 5e-2)
+
+
+POOL_SHAPES = [ConvShape("p64", 2, 64, 20, 22, 64, 3, 3, 1, 1),        # halo mode, ragged tiles
+               ConvShape("p64odd", 1, 64, 17, 13, 64, 3, 3, 1, 1),     # odd P, Q: floor mode drops the tail
+               ConvShape("p128", 2, 128, 16, 18, 128, 3, 3, 1, 1),     # chunked halo mode
+               ConvShape("p64k32", 3, 64, 12, 12, 32, 3, 3, 1, 1, bias=False),
+               ConvShape("p16", 2, 16, 14, 14, 64, 3, 3, 1, 1)]        # 32-byte-pixel halo
+
+
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("shape", POOL_SHAPES, ids=lambda s: s.name)
+def test_fused_maxpool2x2_matches_unfused_bitwise(shape, relu):
+    """conv (+ReLU) -> 2x2 max pooling in the conv epilogue (row f1): the pooled plan's output is
+    bit-identical to ai3_maxpool2d of the plain plan's output, and matches the oracle ops."""
+    import paper_2410_08300_b200 as ai3
+    import paper_2410_08300_b200.layers as L
+    x, w, b = conv_inputs(shape, seed=stable_seed(shape.name), dtype="bf16")
+    xt = _dev(x, "bf16", True)
+    wt, bt = _dev(w, "bf16"), (None if b is None else _dev(b, "bf16"))
+    plain = ai3.ConvPlan(wt, bt, xt.shape, 1, 1, 1, 1, "implicit_gemm", in_layout=1).set_relu(relu)
+    fused = ai3.ConvPlan(wt, bt, xt.shape, 1, 1, 1, 1, "implicit_gemm", in_layout=1).set_relu(relu)
+    fused.set_maxpool2x2(True)
+    assert fused.out_shape == (shape.N, shape.K, shape.P // 2, shape.Q // 2)
+    y = torch.full(fused.out_shape, float("nan"), dtype=torch.bfloat16, device="cuda").contiguous(
+        memory_format=torch.channels_last)
+    fused(xt, out=y)
+    want = L.max_pool2d(plain(xt), 2, 2)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(y).any())
+    assert torch.equal(y, want)
+    ref = oracle.conv2d(_host(xt), _host(wt), None if bt is None else _host(bt), 1, 1, 1)
+    ref = oops.max_pool2d(oops.relu(ref) if relu else ref, 2, 2)
+    assert _rel(_host(y), ref) <= TOL[("bf16", "strict")]
+
+
+def test_fused_maxpool2x2_unsupported_modes_raise():
+    import paper_2410_08300_b200 as ai3
+    x = _dev(np.zeros((2, 256, 12, 12)), "bf16", True)
+    w = _dev(np.zeros((256, 256, 3, 3)), "bf16")
+    p = ai3.ConvPlan(w, None, x.shape, 1, 1, 1, 1, "implicit_gemm", in_layout=1)  # K = 256: im2col mode
+    with pytest.raises(ai3.UnsupportedConfiguration):
+        p.set_maxpool2x2(True)
+    assert p.out_shape == (2, 256, 12, 12)
+    q = ai3.ConvPlan(w, None, x.shape, 1, 1, 1, 1, "direct", in_layout=1)
+    with pytest.raises(ai3.UnsupportedConfiguration):
+        q.set_maxpool2x2(True)
