@@ -250,8 +250,12 @@ def test_swap_backend_vgg16_all_ai3(dtype):
     assert model.kept == []
     kinds = [k for _, k in model.replaced]
     assert kinds.count("fused_relu") == 15 and kinds.count("flatten_fused") == 1
+    assert kinds.count("fused_maxpool2x2") == 5
     with torch.inference_mode():
         y = _host(model(x))
+    if dtype == "bf16":  # conv1_2 and conv2_2 (halo modes) pool in their epilogue
+        pooled = [p for m in model.modules() if isinstance(m, ai3.Conv2D) for _, p in m._plans.values() if p.pool]
+        assert len(pooled) >= 2
     ref = _oracle_vgg16(vgg, _host(x))
     assert _rel(y, ref) <= (1e-4 if dtype == "f32" else 5e-2)
 
