@@ -284,6 +284,7 @@ struct ai3_plan {
     int relu = 0;  // fused ReLU epilogue (ai3_conv2d_plan_set_relu)
     int pool = 0;  // fused 2x2 / stride-2 max pooling (ai3_conv2d_plan_set_maxpool2x2): y is (N, K, P/2, Q/2)
     int cached_out_pool = 0;
+    int ksplit = 1;           // split-K factor (linear-like plans): partials in ws_M, reduced into y
     bool kn_inplace = false;  // kn2row: fp32 NHWC output accumulates in y itself (no workspace)
     int kn_first = -1;        // kn2row: a tap covering every output pixel (runs first, writes), or -1
 };
@@ -517,11 +518,34 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.out_bstride = (long long)T * c.K;
         pl.launches = (pl.need_prep ? 1 : 0) + 3;
     }
+    // split-K for linear-like plans (a 1x1 output map: nn.Linear, flatten -> linear): S K-ranges
+    // whose fp32 partials a reduce pass sums (splitk.cu).  S depends on N and K only -- never on
+    // the batch -- so every output's summation order is the same at any batch size.
+    pl.ksplit = 1;
+    if (algo == AI3_ALGO_IMPLICIT_GEMM && c.P == 1 && c.Q == 1 && a.batch == 1 && c.K % 4 == 0 &&
+        (a.a_mode == TC_A_TILED2D || a.a_mode == TC_A_IM2COL) && knob("AI3_SPLITK", 1)) {
+        const int target = 148 / (int)((c.K + 255) / 256);
+        int S = 1;
+        for (int sx = 2; sx <= target && sx <= a.num_kb / 16; ++sx)
+            if (a.num_kb % sx == 0) S = sx;
+        if (S > 1) {
+            pl.ksplit = S;
+            a.ksplit = S;
+            a.batch = S;
+            a.num_kb /= S;
+            a.out_bf16 = 0;
+            a.out_nchw = 0;
+            a.out_bstride = (long long)M * c.K;
+            pl.ws_M = ws;
+            ws = align_up(ws + (size_t)S * M * c.K * 4);
+            pl.launches += 1;
+        }
+    }
     pl.ws_bytes = ws;
     // TMA-store epilogue for row-major (NHWC / [b][T][K]) outputs whose rows are 16-byte multiples
     const int eo = a.out_bf16 ? 2 : 4;
     a.stg_row = (!a.out_nchw && !a.kn && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
-    a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD && algo != AI3_ALGO_KN2ROW) ? 1 : 0;
+    a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD && algo != AI3_ALGO_KN2ROW && pl.ksplit == 1) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows
     {
@@ -785,6 +809,11 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if (pl.algo == AI3_ALGO_IMPLICIT_GEMM || pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = y;
+        if (pl.ksplit > 1) {  // fp32 partials per K split; bias / ReLU / cast in the reduce pass
+            tp.args.out = w + pl.ws_M;
+            tp.args.bias = nullptr;
+            tp.args.relu = 0;
+        }
     } else if (pl.algo == AI3_ALGO_KN2ROW) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         if (pl.kn_inplace && !aligned(y, 16))
@@ -840,6 +869,11 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if ((s = encode_out_map(pl, tp.args.out)) != AI3_OK) return s;
     e = launch_tc(tp, &pl.ta0, &pl.ta1, &pl.tb0, &pl.tb1, &pl.tout, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 GEMM launch");
+    if (pl.ksplit > 1) {
+        e = launch_splitk_reduce(reinterpret_cast<const float*>(w + pl.ws_M), pl.ksplit, c.N * c.P * c.Q, c.K, bias, y,
+                                 c.dtype == AI3_BF16, pl.relu, st);
+        if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch");
+    }
     if (pl.algo == AI3_ALGO_WINOGRAD) {
         e = launch_winograd_output(w + pl.ws_M, tp.args.out_bf16, tp.args.out_nchw, bias, y, c.out_layout == AI3_NHWC,
                                    c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);

@@ -123,6 +123,9 @@ cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st);
 // KCRS -> [(r*S+s)*K + k][Cpad] rows, compute mode (+ lo).
 cudaError_t launch_pack_weights_kn2row(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
                                        int64_t Cpad, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
+// split-K partials fp32 [S][M][N] -> y[M][N] = cast(ReLU(sum_s part[s] + bias)), s in order.
+cudaError_t launch_splitk_reduce(const float* part, int S, int64_t M, int64_t N, const float* bias, void* y, int bf16,
+                                 int relu, cudaStream_t st);
 // acc fp32 [N*P*Q][K] (the taps' shift-accumulated sums) -> y (+bias, ReLU, cast to y's
 // dtype and layout).  acc == y (fp32 NHWC output accumulated in place) is allowed.
 cudaError_t launch_kn2row_finalize(const float* acc, const float* bias, void* y, int out_nhwc, int bf16, int64_t N,
@@ -199,6 +202,10 @@ struct TcArgs {
     // when both divide and land inside P x Q.  kn = 0 off; 1 read-add-write; 2 write (the
     // first tap, when it covers every output pixel).  b_row_off: first B row of this tap.
     int kn, kn_H, kn_W, kn_oh, kn_ow, b_row_off;
+    // split-K (linear-like plans, 1x1 output map): the "batch" index b of a tile is its K split;
+    // it covers K-blocks [b * num_kb, (b + 1) * num_kb) of the reduction and stores fp32
+    // partial sums to out[b][m][n]; a reduce pass sums the splits in order (kn2row.cu)
+    int ksplit;
     int n2;         // N sub-tiles per unit (1, or 2: one A stage feeds two block_n-column MMAs --
                     // for single-wave layers; bf16 im2col / tiled with the fast epilogue only)
     // gather mode (a_mode == TC_A_GATHER, implicit_precomp_gemm): precomputed input-row table

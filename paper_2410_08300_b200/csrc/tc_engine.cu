@@ -202,11 +202,21 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
             }
         }
         int cc = 0, ts = 0, tr = 0;  // channel chunk, filter column, filter row of the current K-block
+        int kb0 = 0;                 // split-K: first K-block of this tile's split
+        if (a.ksplit > 1) {
+            kb0 = b * a.num_kb;
+            if (a.a_mode == TC_A_IM2COL) {
+                cc = kb0 % a.c_chunks;
+                const int t = kb0 / a.c_chunks;
+                ts = t % a.S;
+                tr = t / a.S;
+            }
+        }
         for (int kb = 0; kb < a.num_kb; ++kb) {
             TRACE_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
             uint8_t* sA = smem + stage * stage_bytes;
             uint8_t* sB = sA + splits * a_bytes;
-            const int kx = kb * kelems;
+            const int kx = (kb0 + kb) * kelems;
             if (a.n2 == 2) {  // one A tile + two B slices (N sub-tiles n0, n0 + block_n); bf16 only
                 const uint16_t ow = (uint16_t)(ts * a.dw), oh = (uint16_t)(tr * a.dh);
                 if (CG == 1) {
@@ -735,9 +745,6 @@ __device__ __forceinline__ void mma_issuer_halo_chunked(const TcArgs& a, uint8_t
     }
 }
 
-// torch.max semantics: NaN propagates (max_pool2d of a NaN window is NaN)
-__device__ __forceinline__ float nan_max(float a, float b) { return (a != a || a > b) ? a : b; }
-
 // ---------------------------------------------------------------- fast epilogue
 // The common case -- bf16 NHWC output through TMA stores, bias (if any) staged in smem,
 // one accumulation chunk per tile -- with every configuration choice resolved at compile
@@ -839,16 +846,24 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
                 }
+                // cast to bf16 pairs
+                __nv_bfloat162 hv[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) hv[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
                 // fused 2x2 / stride-2 max pooling (row f1): in halo tiles TMEM lane = p_l * 8 + q_l,
                 // so a pooling window is lanes {l, l^1, l^8, l^9}; lanes with (l & 9) == 0 keep the
-                // window's max.  bf16 rounding is monotonic, so pooling before the cast is
-                // bit-identical to casting first and pooling after (the unfused model path).
+                // window's max (NaN-propagating, as torch).  Pooling the cast values is what the
+                // unfused path (conv output in bf16, then max_pool2d) computes: identical bits.
                 const bool pooled = HALO && a.pool;
                 if (pooled) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        f[j] = nan_max(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
-                        f[j] = nan_max(f[j], __shfl_xor_sync(0xffffffffu, f[j], 8));
+                    for (int e = 0; e < 16; ++e) {
+                        uint32_t u = *reinterpret_cast<uint32_t*>(&hv[e]);
+                        uint32_t o = __shfl_xor_sync(0xffffffffu, u, 1);
+                        hv[e] = __hmax2_nan(hv[e], *reinterpret_cast<__nv_bfloat162*>(&o));
+                        u = *reinterpret_cast<uint32_t*>(&hv[e]);
+                        o = __shfl_xor_sync(0xffffffffu, u, 8);
+                        hv[e] = __hmax2_nan(hv[e], *reinterpret_cast<__nv_bfloat162*>(&o));
                     }
                 }
                 const int half = BOX64 ? hh : 0;
@@ -863,24 +878,16 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 }
                 if (!pooled) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        __nv_bfloat162 h[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
-                        sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(h));
-                    }
+                    for (int q = 0; q < 4; ++q) sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(&hv[4 * q]));
                 } else if ((lane & 9) == 0) {
                     // pooled pixel (p_l / 2, q_l / 2) of this warp's 2 x 4 block -> staged row pr
                     const int pr = ((lane >> 4) << 2) | ((lane & 7) >> 1);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        __nv_bfloat162 h[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(f[q * 8 + 2 * e], f[q * 8 + 2 * e + 1]);
                         const int qq = q + 4 * half;
                         const uint32_t off = BOX64 ? (uint32_t)(pr * 128 + ((qq ^ (pr & 7)) << 4))
                                                    : (uint32_t)(pr * 64 + ((qq ^ ((pr >> 1) & 3)) << 4));
-                        sts128(buf + off, *reinterpret_cast<uint4*>(h));
+                        sts128(buf + off, *reinterpret_cast<uint4*>(&hv[4 * q]));
                     }
                 }
                 const bool last = col0 + 32 >= a.Ncols;
@@ -1264,7 +1271,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 //    TMA from L2, at the chip's ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch
 //    runs at 11-12 TB/s of TMA loads),
 // plus a per-tile fill / drain.  Partial last waves count at their own size.
-static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups, int cg, int row_bytes, int num_kb) {
+static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups, int cg, int row_bytes, int num_kb,
+                        int rows_real) {
     const int cands[5] = {32, 64, 128, 192, 256};  // 192: K = 192 / 384 layers (AlexNet) without padding
     const double kred_bytes = (double)row_bytes * num_kb;  // bytes of one operand row
     int best = 32;
@@ -1275,10 +1283,15 @@ static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups,
         const long long full = units / num_groups, rest = units % num_groups;
         const double mma_cyc = cg == 2 ? (bn >= 128 ? bn / 2.0 : 46.0) : (bn >= 128 ? bn / 2.0 : 66.5);
         const double t_mma = (double)num_kb * (row_bytes / 32) * mma_cyc;
-        const double tile_bytes = (128.0 * cg + bn) * kred_bytes;
+        const double tile_bytes = ((double)rows_real + bn) * kred_bytes;
         auto wave = [&](long long u) {
             const double t_l2 = u * tile_bytes / 6300.0;
-            return (t_mma > t_l2 ? t_mma : t_l2) + 600.0;
+            // a partial wave leaves SMs idle and each busy one streams its operands at its own
+            // TMA rate (~70 B/clk measured: VGG FC1 at batch 64, 16 CTAs x 16 MB in 114 us)
+            const double t_sm = u < num_groups ? tile_bytes / cg / 70.0 : 0.0;
+            double t = t_mma > t_l2 ? t_mma : t_l2;
+            t = t > t_sm ? t : t_sm;
+            return t + 600.0;
         };
         const double cost = full * wave(num_groups) + (rest ? wave(rest) : 0.0);
         if (best_cost < 0 || cost < best_cost) { best = bn; best_cost = cost; }
@@ -1302,7 +1315,8 @@ void tc_configure(TcPlan& p, int num_sms) {
         a.n2 = 1;
         const int cg = pick_cg(a.M);
         const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
-        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb);
+        const int rows_real = a.M < 128 * cg ? a.M : 128 * cg;  // a lone short M tile loads no padding rows
+        a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb, rows_real);
         // two N sub-tiles per unit when that makes a multi-wave layer fit in one wave (VGG conv5:
         // 98 -> 49 units on 74 CTA pairs): each A stage then feeds 2 x block_n columns, and with
         // one unit per CTA pair the single 512-column TMEM buffer costs no overlap
