@@ -544,7 +544,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
     pl.ws_bytes = ws;
     // TMA-store epilogue for row-major (NHWC / [b][T][K]) outputs whose rows are 16-byte multiples
     const int eo = a.out_bf16 ? 2 : 4;
-    a.stg_row = (!a.out_nchw && !a.kn && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;
+    a.stg_row = (!a.out_nchw && ((int64_t)a.Ncols * eo) % 16 == 0) ? 32 * eo : 0;  // kn2row: 128-byte staging rows
     a.bias_smem = (c.has_bias && algo != AI3_ALGO_WINOGRAD && algo != AI3_ALGO_KN2ROW && pl.ksplit == 1) ? 1 : 0;
     tc_configure(pl.tc, device_num_sms());
     // 128-byte TMA-store rows for bf16 outputs when every N tile is a whole number of 64-column rows

@@ -1075,9 +1075,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];
             }
+            if (a.kn) {
+                if (a.stg_row == 0 || col0 + 32 > a.Ncols || (a.Ncols % 4) != 0) {
+                    kn2row_store(a, f, m_row0 + lane, col0);
+                    return;
+                }
+                // coalesced shift-accumulate: the warp stages its 32 rows x 32 fp32 (swizzled 16-byte
+                // pieces), then 8 lanes per row read-add-write one 128-byte output row segment
+                // (4 rows per instruction) instead of one lane per row
+                int tgt = -1;  // this lane's output pixel (n, p, q) for tap shift, or -1
+                {
+                    const int m = m_row0 + lane;
+                    if (m < a.M) {
+                        const int hw = a.kn_H * a.kn_W;
+                        const int n = m / hw, rem = m - (m / hw) * hw;
+                        const int h = rem / a.kn_W, wq = rem - (rem / a.kn_W) * a.kn_W;
+                        const int pn = h + a.kn_oh, qn = wq + a.kn_ow;
+                        if (pn >= 0 && qn >= 0) {
+                            const int pp = pn / a.sh, qq = qn / a.sw;
+                            if (pp * a.sh == pn && qq * a.sw == qn && pp < a.P && qq < a.Q) tgt = (n * a.P + pp) * a.Q + qq;
+                        }
+                    }
+                }
+                __syncwarp();  // the previous chunk's staged rows have been consumed
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 v4 = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                    sts128(stg_u32 + lane * 128 + ((q ^ (lane & 7)) << 4), *reinterpret_cast<const uint4*>(&v4));
+                }
+                __syncwarp();
+                const int qd = lane & 7;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int r = i * 4 + (lane >> 3);
+                    const int t = __shfl_sync(0xffffffffu, tgt, r);
+                    if (t >= 0) {
+                        const uint4 u = lds128(stg_u32 + r * 128 + ((qd ^ (r & 7)) << 4));
+                        const float4 v = *reinterpret_cast<const float4*>(&u);
+                        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (int64_t)t * a.Ncols +
+                                                                col0) + qd;
+                        if (a.kn == 2) {
+                            *dst = v;
+                        } else {
+                            const float4 o = *dst;
+                            *dst = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+                        }
+                    }
+                }
+                return;
+            }
             if (a.stg_row == 0) {
-                if (a.kn) kn2row_store(a, f, m_row0 + lane, col0);
-                else if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
+                if (row_ok) epilogue_store(a, f, base, cstride, col0, /*bias_added=*/true);
                 return;
             }
             // box64: bf16 rows of 64 channels (128 B) per TMA store -- two 32-column chunks share
