@@ -162,9 +162,10 @@ def test_workspace_sizes():
     assert ws((64, 256, 56, 56), 256, 3, "gemm") >= w_only + 64 * 56 * 56 * 9 * 256 * 2
     # NCHW input adds the layout pass
     assert ws((64, 256, 56, 56), 256, 3, "implicit_gemm", lin=_lib.NCHW) >= w_only + 64 * 56 * 56 * 256 * 2
-    # Winograd: 16 transformed tiles in (V) and out (M, fp32)
+    # Winograd: 16 transformed tiles in (V) and out (M: bf16 for bf16 runs, fp32 otherwise)
     T = 64 * 28 * 28
-    assert ws((64, 256, 56, 56), 256, 3, "winograd") >= 16 * T * 256 * 2 + 16 * T * 256 * 4
+    assert ws((64, 256, 56, 56), 256, 3, "winograd") >= 16 * T * 256 * 2 + 16 * T * 256 * 2
+    assert ws((64, 256, 56, 56), 256, 3, "winograd", dtype=_lib.F32) >= 16 * T * 256 * 4 + 16 * T * 256 * 4
     # direct needs no workspace beyond the fp32 weights [Cg][R][S][K padded to 64] and the fp32
     # bias, each region 256-byte aligned: 3*3*3*64*4 = 6912 (already aligned) + 256
     assert ws((2, 3, 32, 32), 16, 3, "direct", dtype=_lib.F32) == 6912 + 256
