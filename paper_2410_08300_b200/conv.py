@@ -99,8 +99,19 @@ def layout_of(x: torch.Tensor) -> int:
     raise ValueError("input must be contiguous (NCHW) or channels_last (NHWC)")
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def _raw_stream(index: int) -> int:
+    """The current stream's cudaStream_t on device `index` (the hot dispatch path: no Stream
+    object is built)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(index)
+    return torch.cuda.current_stream(index).cuda_stream
 
 
 class _Workspace(threading.local):
@@ -341,6 +352,15 @@ class ConvPlan:
         self.algorithm = algo_name(lib.ai3_conv2d_plan_algo(handle))
         self.workspace_size = int(lib.ai3_conv2d_plan_workspace_size(handle))
         self.num_launches = int(lib.ai3_conv2d_plan_num_launches(handle))
+        self._exec = lib.ai3_conv2d_plan_execute
+        self._set_out_geometry()
+
+    def _set_out_geometry(self):
+        # sizes / strides of the output in the plan's memory format (the hot path allocates it
+        # with one empty_strided call)
+        fmt = torch.channels_last if self.out_layout == _lib.NHWC else torch.contiguous_format
+        probe = torch.empty(self.out_shape, dtype=self.dtype, device="meta", memory_format=fmt)
+        self._out_size, self._out_stride = tuple(probe.shape), probe.stride()
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if tuple(x.shape) != self.in_shape or x.dtype != self.dtype:
@@ -364,6 +384,25 @@ class ConvPlan:
         self._keep = None
         return out
 
+    def run_checked(self, x: torch.Tensor) -> torch.Tensor:
+        """The per-forward hot path of ai3.Conv2D once the module has checked that x has the
+        plan's shape, dtype, device and strides (its memory format): allocate the output and
+        make the one ai3_conv2d_plan_execute call (dispatch adds no overhead)."""
+        dev = self.device
+        out = torch.empty_strided(self._out_size, self._out_stride, dtype=self.dtype, device=dev)
+        sp = _raw_stream(dev.index)
+        ws = None
+        if self.workspace_size:
+            ws = _WS.bufs.get((dev, sp))
+            if ws is None or ws.numel() < self.workspace_size:
+                ws = _WS.get(dev, self.workspace_size)
+        st = self._exec(self._h, x.data_ptr(), out.data_ptr(), None if ws is None else ws.data_ptr(),
+                        0 if ws is None else ws.numel(), sp)
+        if st:
+            _check(st)
+        self._keep = None
+        return out
+
     def set_relu(self, relu: bool = True) -> "ConvPlan":
         """Fuse a ReLU into the plan's output epilogue (ai3_conv2d_plan_set_relu)."""
         _check(_lib.load().ai3_conv2d_plan_set_relu(self._h, 1 if relu else 0))
@@ -378,6 +417,7 @@ class ConvPlan:
         n, k, p, q = self.conv_shape
         self.out_shape = (n, k, p // 2, q // 2) if pool else self.conv_shape
         self.pool = bool(pool)
+        self._set_out_geometry()
         return self
 
     def execute_raw(self, x_ptr: int, y_ptr: int, ws_ptr: int | None, ws_bytes: int, stream_ptr: int):
