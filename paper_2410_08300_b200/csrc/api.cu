@@ -360,8 +360,8 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         // fast or faster)
         const bool allow_c = allow && knob("AI3_HALO_CHUNKED", 1) != 0;
         const bool shape_c = not1x1 && algo == AI3_ALGO_IMPLICIT_GEMM && pl.cm == CM_BF16 && c.sh == 1 && c.sw == 1 &&
-                             c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= 128 && c.K % 8 == 0 &&
-                             c.N <= 65535 && pl.Cpad % 64 == 0 && pl.Cpad >= 128;
+                             c.dh == 1 && c.dw == 1 && c.S <= 9 && c.R <= 32 && c.K <= knob("AI3_HALO_KMAX", 128) &&
+                             c.K <= 256 && c.K % 8 == 0 && c.N <= 65535 && pl.Cpad % 64 == 0 && pl.Cpad >= 128;
         if (allow_c && shape_c) pl.halo_pb = 128;
     }
     pl.taps_pad = pl.halo_pb == 16 ? round_up(c.R * c.S, 2) : c.R * c.S;

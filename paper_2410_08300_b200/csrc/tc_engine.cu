@@ -44,17 +44,35 @@ constexpr int MAX_ACC = 8;          // TMEM accumulator buffers (n_acc * block_n
 }  // namespace
 
 
-// Debug timing trace (AI3_TC_TRACE=1): per-CTA cycle counters of the pipeline waits.
+// Debug timing trace (developer builds only, AI3_TC_TRACE=1): per-CTA cycle counters of the
+// pipeline waits.  The product library compiles every trace statement out.
 //   [0] producer: waiting for a free stage   [1] producer: total
 //   [2] MMA: waiting for operands (full)     [3] MMA: waiting for a drained accumulator
 //   [4] MMA: total                           [5] epilogue warp 2: waiting for an accumulator
 //   [6] epilogue warp 2: total               [7] tiles seen by the epilogue warp 2
-//   [8] epilogue warp 2: tcgen05.ld waits    [9] epilogue warp 2: store_chunk
-//   [10] epilogue warp 2: smem-slot waits (TMA store read)
+//   [8] epilogue warp 2: tcgen05.ld waits    [9] epilogue warp 2: per-tile processing
+//   [10] epilogue warp 2: smem-slot waits (TMA store read)   [11] epilogue: fence + store issue
 __device__ unsigned long long g_tc_trace[296][16];
+#ifdef AI3_DEV_KNOBS
+#define TRACE_ON(a) ((a).trace != 0)
+#else
+#define TRACE_ON(a) false
+#endif
+#define TRACE_CLOCK(a) (TRACE_ON(a) ? clock64() : 0ull)
+// add (clock64() - t0) to counter `slot` from lane 0 of epilogue warp 2
+#define EPI_TRACE_ADD(slot, t0)                                                                  \
+    do {                                                                                         \
+        if (TRACE_ON(a) && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][slot] += clock64() - (t0); \
+    } while (0)
+#define EPI_TRACE(slot, stmt)                                                           \
+    do {                                                                                \
+        const unsigned long long t0__ = TRACE_CLOCK(a);                                 \
+        stmt; /* warp-collective statements stay convergent */                          \
+        EPI_TRACE_ADD(slot, t0__);                                                      \
+    } while (0)
 #define TRACE_WAIT(slot, stmt)                                                          \
     do {                                                                                \
-        if (a.trace) {                                                                  \
+        if (TRACE_ON(a)) {                                                              \
             const unsigned long long t0__ = clock64();                                  \
             stmt;                                                                       \
             g_tc_trace[blockIdx.x][slot] += clock64() - t0__;                           \
@@ -748,8 +766,33 @@ __device__ __forceinline__ void mma_issuer_halo_chunked(const TcArgs& a, uint8_t
 // ---------------------------------------------------------------- fast epilogue
 // The common case -- bf16 NHWC output through TMA stores, bias (if any) staged in smem,
 // one accumulation chunk per tile -- with every configuration choice resolved at compile
-// time, so that each 32-column chunk costs ~70 instructions (the generic path's runtime
-// branches made the epilogue instruction-bound on short-K layers).
+// time or hoisted out of the tile loop.  Per tile and warp: the tile coordinates advance by
+// carries (no division), the TMEM columns leave in pairs of 32-column loads under one wait,
+// and each 64-column box (BOX64) / 32-column box is staged and stored with one TMA store.
+// (Measured, ncu source view of VGG conv1_1: the previous per-chunk loop executed ~490
+// instructions per tile and warp as one dependent chain -- two 64-bit divisions, register
+// shuffles between the prefetch buffers -- and bounded the output-heavy layers.)
+
+// Mixed-radix tile counter (d2, d1, d0), d0 fastest: tile = (d2 * r1 + d1) * r0 + d0, advanced
+// by a fixed stride with carries.
+struct TileWalk {
+    int d0, d1, d2, r0, r1, s0, s1, s2;
+    __device__ __forceinline__ void init(int tile, int stride, int radix0, int radix1) {
+        r0 = radix0; r1 = radix1;
+        d0 = tile % r0; d1 = (tile / r0) % r1; d2 = tile / (r0 * r1);
+        s0 = stride % r0; s1 = (stride / r0) % r1; s2 = stride / (r0 * r1);
+    }
+    __device__ __forceinline__ void step() {
+        d0 += s0;
+        int c = 0;
+        if (d0 >= r0) { d0 -= r0; c = 1; }
+        d1 += s1 + c;
+        c = 0;
+        if (d1 >= r1) { d1 -= r1; c = 1; }
+        d2 += s2 + c;
+    }
+};
+
 template <int CG, bool BOX64, bool HALO>
 __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap& tout, uint64_t* tfull,
                                               uint64_t* tempty, uint32_t tmem_base, uint32_t rank, int unit,
@@ -759,82 +802,94 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
     const int group = (warp - 2) >> 2;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int ncol32 = a.block_n / 32;
-    const int tiles_per_batch = a.m_tiles * a.n_tiles;
-    const int total_tiles = tiles_per_batch * a.batch;
+    const int total_tiles = a.m_tiles * a.n_tiles * a.batch;
     const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     const uint32_t stg_u32 = smem_u32(my_stg);
     const bool has_bias = a.bias != nullptr;
-    // per-lane swizzled 16-byte slot offsets inside a staging buffer
+    const bool relu = a.relu != 0;
+    const bool pooled = HALO && a.pool;
+    // this lane's swizzled 16-byte slot offsets inside a staging buffer (row = lane), and the
+    // pooled variant (row pr = the pooled pixel of this lane's 2 x 2 window, lanes (l & 9) == 0)
+    const int srow = pooled ? (((lane >> 4) << 2) | ((lane & 7) >> 1)) : lane;
     uint32_t qoff[BOX64 ? 8 : 4];
 #pragma unroll
     for (int q = 0; q < (BOX64 ? 8 : 4); ++q)
-        qoff[q] = BOX64 ? (uint32_t)(lane * 128 + ((q ^ (lane & 7)) << 4))
-                        : (uint32_t)(lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4));
+        qoff[q] = BOX64 ? (uint32_t)(srow * 128 + ((q ^ (srow & 7)) << 4))
+                        : (uint32_t)(srow * 64 + ((q ^ ((srow >> 1) & 3)) << 4));
+    const bool writer = !pooled || (lane & 9) == 0;
     int slot = 0, issued = 0;
     const int n_stg = a.n_stg;
     // n2 == 1: the two warpgroups take alternate tiles; n2 == 2: both drain every unit, one
     // N sub-tile each (sub = group)
     const int sub = a.n2 == 2 ? group : 0;
-    int it = -1;
-    for (int tile = unit; tile < total_tiles; tile += num_units) {
-        ++it;
-        if (a.n2 != 2 && (it & 1) != group) continue;
-        const int acc = it % a.n_acc;
-        const uint32_t acc_phase = (uint32_t)((it / a.n_acc) & 1);
-        int n0, row0, qc = 0, img = 0;
+    const bool alternate = a.n2 != 2;
+    TileWalk tw;  // HALO: (image, p band, q band); else (batch, M tile, N tile)
+    if (HALO) tw.init(unit, num_units, a.tiles_q, a.tiles_p);
+    else tw.init(unit, num_units, a.n_tiles, a.m_tiles);
+    int acc = 0, it = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = unit; tile < total_tiles; tile += num_units, ++it) {
+        const int my_acc = acc;
+        const uint32_t my_phase = acc_phase;
+        int n0, row0, qc = 0, img;
         if (HALO) {
-            int hp0;
-            halo_tile(a, tile, CG, rank, img, hp0, qc);
+            img = tw.d2;
+            qc = tw.d0 * a.TQ;
             n0 = 0;
-            row0 = hp0 + quarter * (32 / a.TQ);
+            row0 = (tw.d1 * CG + (int)rank) * a.TP + quarter * (32 / a.TQ);
         } else {
-            img = tile / tiles_per_batch;  // batch index (Winograd's 16 GEMMs) for the 3-D store
-            const int rem = tile - img * tiles_per_batch;
-            const int m0 = (rem / a.n_tiles) * (BM * CG) + (int)rank * BM;
-            n0 = ((rem % a.n_tiles) * a.n2 + sub) * a.block_n;
+            img = tw.d2;  // batch index (Winograd's 16 GEMMs) for the 3-D store
+            const int m0 = tw.d1 * (BM * CG) + (int)rank * BM;
+            n0 = (tw.d0 * a.n2 + sub) * a.block_n;
             row0 = m0 + quarter * 32;
         }
-        mbar_wait(&tfull[acc], acc_phase);
+        tw.step();
+        if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
+        if (alternate && (it & 1) != group) continue;
+        {
+            const unsigned long long tw0 = TRACE_CLOCK(a);
+            mbar_wait(&tfull[my_acc], my_phase);
+            EPI_TRACE_ADD(5, tw0);
+            if (TRACE_ON(a) && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][7] += 1;
+        }
         tc_fence_after();
-        const uint32_t tbase = tmem_base + (acc * a.n2 + sub) * a.block_n + lane_off;
+        const unsigned long long t_tile0 = TRACE_CLOCK(a);
+        const uint32_t tbase = tmem_base + (my_acc * a.n2 + sub) * a.block_n + lane_off;
         // 32-column chunks holding real output channels (the last N tile may be partial: its
         // padding columns are never read, and the TMEM release follows the last real chunk)
         const int nvalid = min(ncol32, (a.Ncols - n0 + 31) / 32);
-        uint32_t va[32], vb[32];
-        tmem_ld32(tbase, va);
         for (int c32 = 0; c32 < nvalid; c32 += 2) {
-            // ---- chunk c32 (even): TMEM -> regs, prefetch c32+1
-            tmem_ld_wait();
-            const bool has_b = c32 + 1 < nvalid;
-            if (has_b) tmem_ld32(tbase + (c32 + 1) * 32, vb);
-            else {
+            const bool two = c32 + 1 < nvalid;
+            uint32_t va[32], vb[32];
+            tmem_ld32(tbase + c32 * 32, va);
+            if (two) tmem_ld32(tbase + (c32 + 1) * 32, vb);
+            EPI_TRACE(8, tmem_ld_wait());
+            if (c32 + 2 >= nvalid) {  // every column of this accumulator is in registers
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
-                    else mbar_arrive_relaxed(&tempty[acc]);
+                    if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + my_acc * 8);
+                    else mbar_arrive_relaxed(&tempty[my_acc]);
                 }
             }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                if (hh == 1) {
-                    if (!has_b) break;
-                    tmem_ld_wait();
-                    if (c32 + 2 < nvalid) tmem_ld32(tbase + (c32 + 2) * 32, va);
-                    else {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
-                            else mbar_arrive_relaxed(&tempty[acc]);
-                        }
-                    }
-                }
-                const uint32_t* v = hh == 0 ? va : vb;
+                if (hh == 1 && !two) break;
                 const int col0 = n0 + (c32 + hh) * 32;
+                const int half = BOX64 ? hh : 0;
+                if (half == 0 && issued >= n_stg) {  // slot reuse: its store must have read smem
+                    const unsigned long long tw0 = TRACE_CLOCK(a);
+                    if (lane == 0) {
+                        if (n_stg == 4) bulk_wait_group_read<3>();
+                        else if (n_stg == 2) bulk_wait_group_read<1>();
+                        else bulk_wait_group_read<0>();
+                    }
+                    __syncwarp();
+                    EPI_TRACE_ADD(10, tw0);
+                }
                 float f[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(hh == 0 ? va[j] : vb[j]);
                 if (has_bias) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
@@ -842,56 +897,42 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                         f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
                     }
                 }
-                if (a.relu) {
+                if (relu) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
                 }
-                // cast to bf16 pairs
-                __nv_bfloat162 hv[16];
+                uint32_t hv[16];  // bf16 pairs
 #pragma unroll
-                for (int e = 0; e < 16; ++e) hv[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+                for (int e = 0; e < 16; ++e) {
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+                    hv[e] = *reinterpret_cast<uint32_t*>(&h2);
+                }
                 // fused 2x2 / stride-2 max pooling (row f1): in halo tiles TMEM lane = p_l * 8 + q_l,
                 // so a pooling window is lanes {l, l^1, l^8, l^9}; lanes with (l & 9) == 0 keep the
                 // window's max (NaN-propagating, as torch).  Pooling the cast values is what the
                 // unfused path (conv output in bf16, then max_pool2d) computes: identical bits.
-                const bool pooled = HALO && a.pool;
                 if (pooled) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        uint32_t u = *reinterpret_cast<uint32_t*>(&hv[e]);
-                        uint32_t o = __shfl_xor_sync(0xffffffffu, u, 1);
-                        hv[e] = __hmax2_nan(hv[e], *reinterpret_cast<__nv_bfloat162*>(&o));
-                        u = *reinterpret_cast<uint32_t*>(&hv[e]);
-                        o = __shfl_xor_sync(0xffffffffu, u, 8);
-                        hv[e] = __hmax2_nan(hv[e], *reinterpret_cast<__nv_bfloat162*>(&o));
+                        uint32_t o = __shfl_xor_sync(0xffffffffu, hv[e], 1);
+                        __nv_bfloat162 m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[e]),
+                                                        *reinterpret_cast<__nv_bfloat162*>(&o));
+                        hv[e] = *reinterpret_cast<uint32_t*>(&m2);
+                        o = __shfl_xor_sync(0xffffffffu, hv[e], 8);
+                        m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[e]),
+                                         *reinterpret_cast<__nv_bfloat162*>(&o));
+                        hv[e] = *reinterpret_cast<uint32_t*>(&m2);
                     }
                 }
-                const int half = BOX64 ? hh : 0;
                 const uint32_t buf = stg_u32 + slot * 32 * ROWB;
-                if (half == 0 && issued >= n_stg) {  // slot reuse: that store must have read smem
-                    if (lane == 0) {
-                        if (n_stg == 4) bulk_wait_group_read<3>();
-                        else if (n_stg == 2) bulk_wait_group_read<1>();
-                        else bulk_wait_group_read<0>();
-                    }
-                    __syncwarp();
-                }
-                if (!pooled) {
+                if (writer) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) sts128(buf + qoff[q + 4 * half], *reinterpret_cast<uint4*>(&hv[4 * q]));
-                } else if ((lane & 9) == 0) {
-                    // pooled pixel (p_l / 2, q_l / 2) of this warp's 2 x 4 block -> staged row pr
-                    const int pr = ((lane >> 4) << 2) | ((lane & 7) >> 1);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int qq = q + 4 * half;
-                        const uint32_t off = BOX64 ? (uint32_t)(pr * 128 + ((qq ^ (pr & 7)) << 4))
-                                                   : (uint32_t)(pr * 64 + ((qq ^ ((pr >> 1) & 3)) << 4));
-                        sts128(buf + off, *reinterpret_cast<uint4*>(&hv[4 * q]));
-                    }
+                    for (int q = 0; q < 4; ++q)
+                        sts128(buf + qoff[q + 4 * half],
+                               make_uint4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]));
                 }
-                const bool last = col0 + 32 >= a.Ncols;
-                if (BOX64 && half == 0 && !last) continue;
+                if (BOX64 && half == 0 && two) continue;  // the odd chunk fills the box's second half
+                const unsigned long long t_st0 = TRACE_CLOCK(a);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -903,10 +944,12 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                     else tma_store_2d(&tout, src, cx, row0);
                     bulk_commit_group();
                 }
+                EPI_TRACE_ADD(11, t_st0);
                 ++issued;
                 if (++slot == n_stg) slot = 0;
             }
         }
+        EPI_TRACE_ADD(9, t_tile0);
     }
     if (lane == 0) bulk_wait_group<0>();
     __syncwarp();
@@ -977,7 +1020,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // MMA issuer (leader CTA only); the inner loops are specialised on the operand
         // kind and on the number of 32-byte K slices per K-block (1, 2 or 4).
         const bool elected = elect_one();  // one elect.sync for the whole warp
-        const unsigned long long t_mma0 = clock64();
+        const unsigned long long t_mma0 = TRACE_CLOCK(a);
         if (leader && elected && a.a_mode == TC_A_HALO && a.halo_chunks > 1) {
             mma_issuer_halo_chunked<CG>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
         } else if (leader && elected && a.a_mode == TC_A_HALO) {
@@ -1001,10 +1044,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else mma_issuer<CG, CM_3XTF32, 1>(a, smem, full, empty, tfull, tempty, tmem_base, unit, num_units);
             }
         }
-        if (a.trace && leader && elected) g_tc_trace[blockIdx.x][4] += clock64() - t_mma0;
+        if (TRACE_ON(a) && leader && elected) g_tc_trace[blockIdx.x][4] += clock64() - t_mma0;
         __syncwarp();
     } else {
-        const unsigned long long t_epi0 = clock64();
+        const unsigned long long t_epi0 = TRACE_CLOCK(a);
         // ------------------------------------------------------------ epilogue (warps 2..5)
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int group = (warp - 2) >> 2;  // epilogue warpgroup: takes every other tile
@@ -1025,7 +1068,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             named_bar_sync(1, 32 * NUM_EPI_WARPS);
         }
         const bool fast = nchunks == 1 && a.out_bf16 && !a.out_nchw && a.stg_row != 0 &&
-                          (a.bias == nullptr || a.bias_smem) && !a.trace &&
+                          (a.bias == nullptr || a.bias_smem) &&
                           (a.n_stg == 1 || a.n_stg == 2 || a.n_stg == 4) && a.epi_fast;
         // invariant: N sub-tiles are configured for the fast epilogue only (tc_configure), and
         // execute() rejects outputs that would turn the TMA stores off for such a plan
@@ -1134,7 +1177,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int slot = nstore % a.n_stg;
             const uint32_t buf = stg_u32 + slot * 32 * a.stg_row;
             if (nstore >= a.n_stg && half == 0) {  // the store that used this slot must have read it
-                const unsigned long long tw0 = a.trace ? clock64() : 0ull;
+                const unsigned long long tw0 = TRACE_CLOCK(a);
                 if (lane == 0) {
                     if (a.n_stg == 8) bulk_wait_group_read<7>();
                     else if (a.n_stg == 4) bulk_wait_group_read<3>();
@@ -1142,7 +1185,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     else bulk_wait_group_read<0>();
                 }
                 __syncwarp();
-                if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][10] += clock64() - tw0;
+                if (TRACE_ON(a) && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][10] += clock64() - tw0;
             }
             if (a.out_bf16 && a.box64) {  // 128-byte rows, SWIZZLE_128B: piece q of row r at q ^ (r & 7)
 #pragma unroll
@@ -1231,7 +1274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             if (nchunks == 1) {
-                if (warp == 2) { TRACE_WAIT(5, mbar_wait(&tfull[acc], acc_phase)); if (a.trace && lane == 0) g_tc_trace[blockIdx.x][7] += 1; }
+                if (warp == 2) { TRACE_WAIT(5, mbar_wait(&tfull[acc], acc_phase)); if (TRACE_ON(a) && lane == 0) g_tc_trace[blockIdx.x][7] += 1; }
                 else mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 // software-pipelined: the TMEM load of chunk c+1 is in flight while chunk c is stored
@@ -1297,7 +1340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
         if (lane == 0 && a.stg_row != 0) bulk_wait_group<0>();  // smem must outlive the last TMA stores
-        if (a.trace && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][6] += clock64() - t_epi0;
+        if (TRACE_ON(a) && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][6] += clock64() - t_epi0;
         __syncwarp();
     }
     tc_fence_before();
@@ -1312,31 +1355,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ---------------------------------------------------------------- host side
 
 // N tile: the candidate with the least modelled time.  Per wave of concurrently running
-// tiles the time is the larger of
+// tiles the time is the largest of
 //  * the tensor pipe: K-blocks x 32-byte K slices x cycles per MMA (measured tcgen05 rates,
-//    128xNx16 / 256xNx16 cost max(N/2, ~66 / ~46) cycles), and
-//  * the operand stream of that wave: every tile brings its A rows and its B slice through
-//    TMA from L2, at the chip's ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch
-//    runs at 11-12 TB/s of TMA loads),
-// plus a per-tile fill / drain.  Partial last waves count at their own size.
+//    128xNx16 / 256xNx16 cost max(N/2, ~66 / ~46) cycles),
+//  * the chip's operand stream: every tile brings its A rows and its B slice through TMA
+//    from L2 at ~6300 B/clk (DESIGN.md §6 "Roofline": every measured launch runs at
+//    11-12 TB/s of TMA loads), and
+//  * one SM's operand stream: ~42.5 B/clk per SM whether or not the wave is full (measured:
+//    VGG conv5_2's partial second wave of 24 CTA pairs at bn = 256 took as long as a full
+//    one, 2.36 MB per CTA in 28 us),
+// plus a per-tile fill / drain.  Partial last waves count at their own size.  The last N tile
+// may be partial (its B rows past Ncols are TMA zero fill, its columns are never stored):
+// bn = 192 runs a 512-column layer as 3 tiles, which on 49 M tiles is two full waves of 74
+// CTA pairs instead of one and a third (VGG conv5: 57 -> 50 us measured).
 static int pick_block_n(int Ncols, long long m_units, int batch, int num_groups, int cg, int row_bytes, int num_kb,
                         int rows_real) {
-    const int cands[5] = {32, 64, 128, 192, 256};  // 192: K = 192 / 384 layers (AlexNet) without padding
+    const int cands[5] = {32, 64, 128, 192, 256};
     const double kred_bytes = (double)row_bytes * num_kb;  // bytes of one operand row
     int best = 32;
     double best_cost = -1;
     for (int bn : cands) {
-        if (bn == 192 && Ncols % 192 != 0) continue;
+        if (bn > 32 && Ncols <= bn / 2) continue;  // more than half of the tile would be padding
         const long long units = m_units * ((Ncols + bn - 1) / bn) * batch;
         const long long full = units / num_groups, rest = units % num_groups;
         const double mma_cyc = cg == 2 ? (bn >= 128 ? bn / 2.0 : 46.0) : (bn >= 128 ? bn / 2.0 : 66.5);
         const double t_mma = (double)num_kb * (row_bytes / 32) * mma_cyc;
         const double tile_bytes = ((double)rows_real + bn) * kred_bytes;
+        const double t_sm = tile_bytes / cg / 42.5;
         auto wave = [&](long long u) {
             const double t_l2 = u * tile_bytes / 6300.0;
-            // a partial wave leaves SMs idle and each busy one streams its operands at its own
-            // TMA rate (~70 B/clk measured: VGG FC1 at batch 64, 16 CTAs x 16 MB in 114 us)
-            const double t_sm = u < num_groups ? tile_bytes / cg / 70.0 : 0.0;
             double t = t_mma > t_l2 ? t_mma : t_l2;
             t = t > t_sm ? t : t_sm;
             return t + 600.0;
@@ -1383,7 +1430,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     a.cg = pick_cg(a.M);
     a.epi_fast = knob("AI3_EPI_FAST", 1) != 0;
     a.trace = knob("AI3_TC_TRACE", 0) != 0;
-    if (a.n2 == 2 && (!a.epi_fast || a.trace)) a.n2 = 1;  // N sub-tiles run in the fast epilogue only
+    if (a.n2 == 2 && !a.epi_fast) a.n2 = 1;  // N sub-tiles run in the fast epilogue only
     a.pf_tiles = knob("AI3_PF", 0);  // L2 prefetch distance in scheduler steps (TILED2D)
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const bool chunked = a.a_mode == TC_A_HALO && a.halo_chunks > 1;

@@ -32,7 +32,7 @@ METRICS = {"gpu__time_duration.sum": "us", "sm__cycles_elapsed.avg.per_second": 
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
            "sm__warps_active.avg.pct_of_peak_sustained_active": "occ_pct"}
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+SCALE = {"s": 1e6, "ms": 1e3, "us": 1, "ns": 1e-3, "second": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
          "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "cycle/second": 1, "cycle/nsecond": 1e9, "cycle/usecond": 1e6}
 
 

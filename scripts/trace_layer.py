@@ -4,8 +4,9 @@ os.environ["AI3_TC_TRACE"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np, torch
-import paper_2410_08300_b200 as ai3
 from paper_2410_08300_b200 import _lib
+_lib.select_library(os.path.join(ROOT, "paper_2410_08300_b200", "libai3_dev.so"))  # knobs (AI3_TC_TRACE) need the dev build
+import paper_2410_08300_b200 as ai3
 from synth import workload, conv_inputs
 net = sys.argv[2] if len(sys.argv) > 2 else "vgg16"
 spec = [l for l in workload(net) if l.name == sys.argv[1]][0]
@@ -21,7 +22,7 @@ lib.ai3_debug_tc_trace(buf.ctypes.data, 296)  # reset
 p(x, out=y); torch.cuda.synchronize()
 lib.ai3_debug_tc_trace(buf.ctypes.data, 296)
 rows = buf[buf[:, 6] > 0].astype(np.float64)
-names = ["prod_wait_empty", "prod_total", "mma_wait_full", "mma_wait_tempty", "mma_total", "epi_wait_tfull", "epi_total", "epi_tiles", "epi_ld_wait", "epi_store_chunk", "epi_slot_wait"]
+names = ["prod_wait_empty", "prod_total", "mma_wait_full", "mma_wait_tempty", "mma_total", "epi_wait_tfull", "epi_total", "epi_tiles", "epi_ld_wait", "epi_tile_proc", "epi_slot_wait", "epi_fence_store", "epi_fence", "epi_release"]
 print(spec.name, p.algorithm, "ctas", len(rows))
 for i, n in enumerate(names):
     col = rows[:, i]
