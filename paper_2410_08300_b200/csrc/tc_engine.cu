@@ -822,30 +822,37 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
     // n2 == 1: the two warpgroups take alternate tiles; n2 == 2: both drain every unit, one
     // N sub-tile each (sub = group)
     const int sub = a.n2 == 2 ? group : 0;
+    // warpgroup g drains the scheduler's tiles g, g + 2, ... of this CTA (n2 == 1; the
+    // accumulator count is even then) or every tile (n2 == 2): it walks its own tiles only
+    const int n_acc = a.n_acc;
     const bool alternate = a.n2 != 2;
+    const int first = alternate ? unit + group * num_units : unit;
+    const int stride = alternate ? 2 * num_units : num_units;
+    const int acc_step = alternate ? 2 : 1;
+    const int TQ = a.TQ, TP = a.TP, rows_per_warp = 32 / a.TQ, block_n = a.block_n, Ncols = a.Ncols, n2 = a.n2;
     TileWalk tw;  // HALO: (image, p band, q band); else (batch, M tile, N tile)
-    if (HALO) tw.init(unit, num_units, a.tiles_q, a.tiles_p);
-    else tw.init(unit, num_units, a.n_tiles, a.m_tiles);
-    int acc = 0, it = 0;
+    if (HALO) tw.init(first, stride, a.tiles_q, a.tiles_p);
+    else tw.init(first, stride, a.n_tiles, a.m_tiles);
+    int acc = alternate ? group : 0;
     uint32_t acc_phase = 0;
-    for (int tile = unit; tile < total_tiles; tile += num_units, ++it) {
+    for (int tile = first; tile < total_tiles; tile += stride) {
         const int my_acc = acc;
         const uint32_t my_phase = acc_phase;
         int n0, row0, qc = 0, img;
         if (HALO) {
             img = tw.d2;
-            qc = tw.d0 * a.TQ;
+            qc = tw.d0 * TQ;
             n0 = 0;
-            row0 = (tw.d1 * CG + (int)rank) * a.TP + quarter * (32 / a.TQ);
+            row0 = (tw.d1 * CG + (int)rank) * TP + quarter * rows_per_warp;
         } else {
             img = tw.d2;  // batch index (Winograd's 16 GEMMs) for the 3-D store
             const int m0 = tw.d1 * (BM * CG) + (int)rank * BM;
-            n0 = (tw.d0 * a.n2 + sub) * a.block_n;
+            n0 = (tw.d0 * n2 + sub) * block_n;
             row0 = m0 + quarter * 32;
         }
         tw.step();
-        if (++acc == a.n_acc) { acc = 0; acc_phase ^= 1; }
-        if (alternate && (it & 1) != group) continue;
+        acc += acc_step;
+        if (acc >= n_acc) { acc -= n_acc; acc_phase ^= 1; }
         {
             const unsigned long long tw0 = TRACE_CLOCK(a);
             mbar_wait(&tfull[my_acc], my_phase);
@@ -854,23 +861,57 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
         }
         tc_fence_after();
         const unsigned long long t_tile0 = TRACE_CLOCK(a);
-        const uint32_t tbase = tmem_base + (my_acc * a.n2 + sub) * a.block_n + lane_off;
+        const uint32_t tbase = tmem_base + (my_acc * n2 + sub) * block_n + lane_off;
         // 32-column chunks holding real output channels (the last N tile may be partial: its
         // padding columns are never read, and the TMEM release follows the last real chunk)
-        const int nvalid = min(ncol32, (a.Ncols - n0 + 31) / 32);
+        const int nvalid = min(ncol32, (Ncols - n0 + 31) / 32);
+        // columns leave TMEM in pairs of 32-column loads; the next pair's loads are in flight
+        // while the current pair is staged and stored
+        uint32_t va[32], vb[32];
+        tmem_ld32(tbase, va);
+        if (nvalid > 1) tmem_ld32(tbase + 32, vb);
         for (int c32 = 0; c32 < nvalid; c32 += 2) {
             const bool two = c32 + 1 < nvalid;
-            uint32_t va[32], vb[32];
-            tmem_ld32(tbase + c32 * 32, va);
-            if (two) tmem_ld32(tbase + (c32 + 1) * 32, vb);
+            const bool last_pair = c32 + 2 >= nvalid;
             EPI_TRACE(8, tmem_ld_wait());
-            if (c32 + 2 >= nvalid) {  // every column of this accumulator is in registers
+            tmem_regs_after_wait(va);
+            tmem_regs_after_wait(vb);
+            if (last_pair) {  // every column of this accumulator is in registers
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + my_acc * 8);
                     else mbar_arrive_relaxed(&tempty[my_acc]);
                 }
+            }
+            uint32_t hv[2][16];  // bf16 pairs of the two chunks
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh == 1 && !two) break;
+                const int col0 = n0 + (c32 + hh) * 32;
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(hh == 0 ? va[j] : vb[j]);
+                if (has_bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 bv = lds128f(sbias_u32 + (col0 + j) * 4);
+                        f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
+                    }
+                }
+                if (relu) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
+                }
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+                    hv[hh][e] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+            }
+            if (!last_pair) {  // prefetch the next pair (va / vb are consumed)
+                tmem_ld32(tbase + (c32 + 2) * 32, va);
+                if (c32 + 3 < nvalid) tmem_ld32(tbase + (c32 + 3) * 32, vb);
             }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
@@ -887,26 +928,6 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                     __syncwarp();
                     EPI_TRACE_ADD(10, tw0);
                 }
-                float f[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(hh == 0 ? va[j] : vb[j]);
-                if (has_bias) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const float4 bv = lds128f(sbias_u32 + (col0 + j) * 4);
-                        f[j] += bv.x; f[j + 1] += bv.y; f[j + 2] += bv.z; f[j + 3] += bv.w;
-                    }
-                }
-                if (relu) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) f[j] = f[j] < 0.f ? 0.f : f[j];  // NaN passes (torch.relu)
-                }
-                uint32_t hv[16];  // bf16 pairs
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    __nv_bfloat162 h2 = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
-                    hv[e] = *reinterpret_cast<uint32_t*>(&h2);
-                }
                 // fused 2x2 / stride-2 max pooling (row f1): in halo tiles TMEM lane = p_l * 8 + q_l,
                 // so a pooling window is lanes {l, l^1, l^8, l^9}; lanes with (l & 9) == 0 keep the
                 // window's max (NaN-propagating, as torch).  Pooling the cast values is what the
@@ -914,14 +935,14 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
                 if (pooled) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        uint32_t o = __shfl_xor_sync(0xffffffffu, hv[e], 1);
-                        __nv_bfloat162 m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[e]),
+                        uint32_t o = __shfl_xor_sync(0xffffffffu, hv[hh][e], 1);
+                        __nv_bfloat162 m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[hh][e]),
                                                         *reinterpret_cast<__nv_bfloat162*>(&o));
-                        hv[e] = *reinterpret_cast<uint32_t*>(&m2);
-                        o = __shfl_xor_sync(0xffffffffu, hv[e], 8);
-                        m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[e]),
+                        hv[hh][e] = *reinterpret_cast<uint32_t*>(&m2);
+                        o = __shfl_xor_sync(0xffffffffu, hv[hh][e], 8);
+                        m2 = __hmax2_nan(*reinterpret_cast<__nv_bfloat162*>(&hv[hh][e]),
                                          *reinterpret_cast<__nv_bfloat162*>(&o));
-                        hv[e] = *reinterpret_cast<uint32_t*>(&m2);
+                        hv[hh][e] = *reinterpret_cast<uint32_t*>(&m2);
                     }
                 }
                 const uint32_t buf = stg_u32 + slot * 32 * ROWB;
@@ -929,7 +950,7 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         sts128(buf + qoff[q + 4 * half],
-                               make_uint4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]));
+                               make_uint4(hv[hh][4 * q], hv[hh][4 * q + 1], hv[hh][4 * q + 2], hv[hh][4 * q + 3]));
                 }
                 if (BOX64 && half == 0 && two) continue;  // the odd chunk fills the box's second half
                 const unsigned long long t_st0 = TRACE_CLOCK(a);
@@ -1499,6 +1520,9 @@ void tc_configure(TcPlan& p, int num_sms) {
     }
     if (a.n_acc < 2 && a.n2 == 1) a.n_acc = 2;
     if (a.n_acc < 1) a.n_acc = 1;  // n2 == 2 at BLOCK_N = 256: one 512-column buffer
+    // the two epilogue warpgroups take alternate tiles (n2 == 1): an even buffer count keeps
+    // each group on its own buffers (epilogue_fast steps its accumulator index by 2)
+    if (a.n2 == 1 && (a.n_acc & 1)) a.n_acc -= 1;
     int cols = 32;
     while (cols < a.n_acc * a.block_n * a.n2) cols *= 2;
     p.tmem_cols = cols;
