@@ -1017,6 +1017,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch (launch_tc): the setup above overlapped the previous
+    // kernel's tail; every global read / write below (bias, operands, outputs) follows its
+    // completion
+    griddep_launch_dependents();
+    griddep_wait();
 
     const int tiles_per_batch = a.m_tiles * a.n_tiles;
     const int total_tiles = tiles_per_batch * a.batch;
@@ -1561,22 +1566,27 @@ cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap*
     const CUtensorMap& A1 = a1 ? *a1 : *a0;
     const CUtensorMap& B1 = b1 ? *b1 : *b0;
     const CUtensorMap& O = out ? *out : *a0;  // unused by the kernel unless args.stg_row != 0
-    if (p.args.cg == 1) {
-        tc_gemm_kernel<1><<<p.grid, NUM_THREADS, p.smem_bytes, st>>>(*a0, A1, *b0, B1, O, p.args, p.tmem_cols);
-        return cudaGetLastError();
-    }
+    // programmatic stream serialization: the kernel's prologue (barrier init, TMEM allocation,
+    // descriptor prefetch) may run while the previous kernel in the stream drains; the kernel
+    // waits (griddepcontrol.wait) for that kernel's completion before any global access
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    if (p.args.cg == 1) {
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<1>, *a0, A1, *b0, B1, O, p.args, p.tmem_cols);
+    }
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, *a0, A1, *b0, B1, O, p.args, p.tmem_cols);
 }
 
