@@ -217,6 +217,25 @@ def test_swap_backend_convnet_all_ai3(graph):
     assert _rel(_host(y), ref) <= 1e-5
 
 
+@pytest.mark.parametrize("sel,tol", [("direct", 1e-5), ("smm", 1e-5), ("gemm", 1e-5), ("implicit_gemm", 1e-5),
+                                     ("implicit_precomp_gemm", 1e-5), ("kn2row", 1e-5), ("winograd", 1e-3),
+                                     ("guess", 1e-5), (["direct", "winograd"], 1e-3)])
+def test_swap_conv2d_convnet_vs_composed_oracle(sel, tol):
+    """swap_conv2d: only the convolutions run in ai3, ReLU / pooling /
+    flatten stay PyTorch's (fp32).  Compared with the model composed from oracle ops (fp64)
+    on the same parameters and input (randn(10, 3, 224, 224))."""
+    import paper_2410_08300_b200 as ai3
+    torch.manual_seed(0)
+    orig = ConvNet().cuda()
+    x = torch.randn(10, 3, 224, 224, device="cuda")
+    ref = _oracle_convnet(orig, _host(x))
+    model = ai3.swap_conv2d(orig, sel)
+    assert [type(model.conv1).__name__, type(model.conv2).__name__] == ["Conv2D", "Conv2D"]
+    with torch.inference_mode():
+        y = model(x)
+    assert _rel(_host(y), ref) <= tol
+
+
 def _oracle_vgg16(vgg, x):
     """VGG-16 forward composed from oracle ops (fp64), on the model's own parameters."""
     y = x
