@@ -439,6 +439,9 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.c_chunks = (int)(pl.Cpad * pl.elem / a.row_bytes);
         a.num_kb = (int)(c.R * c.S * a.c_chunks);
         a.gather_rows = (int)pl.idx_rows;
+        // 128-byte K-block rows: cp.async gather (16 bytes per lane); narrower rows: TMA gather4
+        a.ga_async = (a.row_bytes == 128 && knob("AI3_GATHER_ASYNC", 1)) ? 1 : 0;
+        a.ga_pitch = (int)(pl.Cpad * pl.elem);
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_GEMM && c.R == 1 && c.S == 1 && c.sh == 1 && c.sw == 1 && c.ph == 0 &&
                c.pw == 0) {
@@ -809,6 +812,8 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
     if (pl.algo == AI3_ALGO_IMPLICIT_GEMM || pl.algo == AI3_ALGO_IMPLICIT_PRECOMP_GEMM) {
         if ((s = encode_a_maps(pl, xs, xs_lo)) != AI3_OK) return s;
         tp.args.out = y;
+        tp.args.ga_src = reinterpret_cast<const char*>(xs);
+        tp.args.ga_src_lo = reinterpret_cast<const char*>(xs_lo);
         if (pl.ksplit > 1) {  // fp32 partials per K split; bias / ReLU / cast in the reduce pass
             tp.args.out = w + pl.ws_M;
             tp.args.bias = nullptr;

@@ -212,6 +212,14 @@ struct TcArgs {
     // [R*S][m_rows] int32 (row of the NHWC [N*H*W][Cpad] view, -1 = padding -> zero fill)
     const int* gather_idx;
     int gather_rows;  // m_rows: the table's row pitch (>= m_tiles * 128 * cg)
+    // ga_async = 1 (128-byte K-block rows): the producer warp gathers the A rows with
+    // cp.async (16 bytes per lane, 8 lanes per row, SWIZZLE_128B addresses computed in the
+    // kernel) instead of one TMA gather4 per 4 rows; ga_src / ga_src_lo: the NHWC operand rows
+    // [N*H*W][ga_pitch bytes] (3xTF32: hi / lo parts)
+    int ga_async;
+    int ga_pitch;
+    const char* ga_src;
+    const char* ga_src_lo;
     const float* bias;  // fp32 [Ncols] or null
     void* out;
     long long out_bstride;  // elements between batches

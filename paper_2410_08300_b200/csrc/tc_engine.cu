@@ -371,6 +371,74 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
     }
 }
 
+// ---------------------------------------------------------------- gather producer, cp.async (one warp)
+// ga_async (single-CTA tiles): the A tile of K-block (tap, chunk) -- 128 table-named rows x
+// 128 bytes -- moves with cp.async: 8 lanes per row (one 16-byte chunk each, its
+// SWIZZLE_128B slot (c ^ row % 8) computed here), 4 rows per warp instruction, zero fill for
+// rows of -1; the B slice still comes by TMA.  Every lane then arms a cp.async.mbarrier
+// arrive on the stage's full barrier, which counts B's transaction bytes plus the 32 lane
+// arrivals, so the producer never waits for its own copies.  The MMA thread fences the
+// generic -> async proxy after acquiring the barrier (the tensor core reads smem through the
+// async proxy).  (Measured: one TMA gather4 per 4 rows issued ~1 per 87 cycles per SM, so the
+// gather4 producer ran VGG conv3_2 at 0.13 of the tensor rate.)
+__device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUtensorMap& tb0, const CUtensorMap& tb1,
+                                                      uint8_t* smem, uint64_t* full, uint64_t* empty, int unit,
+                                                      int num_units, int lane) {
+    const int splits = a.cm == CM_3XTF32 ? 2 : 1;
+    const uint32_t a_bytes = BM * 128u, b_bytes = (uint32_t)a.block_n * 128u;
+    const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
+    const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
+    const int tiles_per_batch = a.m_tiles * a.n_tiles;
+    const uint32_t s0 = smem_u32(smem);
+    const int taps = a.num_kb / a.c_chunks;
+    const int sub_row = lane >> 3, chunk = lane & 7;  // row within a 4-row group, 16-byte chunk
+    // table entries of rows lane, lane + 32, lane + 64, lane + 96 of (tile, tap)
+    auto rows_of = [&](int tile, int tap) -> int4 {
+        const int m0 = (tile / a.n_tiles) * BM;
+        const int* t = a.gather_idx + (size_t)tap * a.gather_rows + m0 + lane;
+        return make_int4(__ldg(t), __ldg(t + 32), __ldg(t + 64), __ldg(t + 96));
+    };
+    int stage = 0;
+    uint32_t phase = 0;
+    int4 r_cur = unit < tiles_per_batch ? rows_of(unit, 0) : make_int4(-1, -1, -1, -1);
+    for (int tile = unit; tile < tiles_per_batch; tile += num_units) {
+        const int mt = tile / a.n_tiles;
+        const int n0 = (tile - mt * a.n_tiles) * a.block_n;
+        int cc = 0, tap = 0;
+        int4 r_next = r_cur;
+        for (int kb = 0; kb < a.num_kb; ++kb) {
+            if (cc == 0) {  // prefetch the next tap's rows (or the next tile's first tap)
+                if (tap + 1 < taps) r_next = rows_of(tile, tap + 1);
+                else if (tile + num_units < tiles_per_batch) r_next = rows_of(tile + num_units, 0);
+            }
+            if (lane == 0) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], splits * b_bytes);
+                uint8_t* sB = smem + stage * stage_bytes + splits * a_bytes;
+                tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
+                if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
+            }
+            __syncwarp();
+            const uint32_t sA = s0 + stage * stage_bytes;
+            const size_t col = (size_t)cc * 128 + chunk * 16;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3; this lane: row 4j + sub_row, chunk
+                const int row = 4 * j + sub_row;
+                const int reg = row >> 5;
+                const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
+                const int idx = __shfl_sync(0xffffffffu, rv, row & 31);
+                const uint32_t dst = sA + row * 128 + ((chunk ^ (row & 7)) << 4);
+                const size_t off = (size_t)(idx < 0 ? 0 : idx) * a.ga_pitch + col;
+                cp_async16(dst, a.ga_src + off, idx < 0 ? 0u : 16u);
+                if (splits == 2) cp_async16(dst + a_bytes, a.ga_src_lo + off, idx < 0 ? 0u : 16u);
+            }
+            cp_async_mbar_arrive_noinc(&full[stage]);
+            if (++cc == a.c_chunks) { cc = 0; ++tap; r_cur = r_next; }
+            if (++stage == a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- MMA issuer (one thread)
 // The K loop of a tile is split into accumulation chunks of `promote_kb` K-blocks (the
 // whole loop unless 3xTF32); each chunk goes to one of the two TMEM buffers and is handed
@@ -404,6 +472,7 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
                 d_tmem = tmem_base + acc * a.block_n * a.n2;
             }
             TRACE_WAIT(2, mbar_wait(&full[stage], phase));
+            if (a.ga_async) fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tensor core reads
             tc_fence_after();
             const uint64_t soff = (uint64_t)((stage * stage_bytes) >> 4);
             const uint64_t ad = a_desc0 + soff, bd = b_desc0 + soff;
@@ -1003,7 +1072,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_prefetch_desc(&ta0);
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
-        for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        // cp.async gather: B's transaction bytes + one arrival per CTA's A rows
+        const uint32_t full_count = (a.a_mode == TC_A_GATHER && a.ga_async) ? 1 + 32 : 1;
+        for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], full_count); mbar_init(&empty[s], 1); }
         // n2 == 2: both epilogue warpgroups drain every accumulator (one N sub-tile each)
         for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG * a.n2); }
         mbar_init(bres, 1);
@@ -1029,7 +1100,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int unit = blockIdx.x / CG, num_units = gridDim.x / CG;  // tile scheduler works per CTA group
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
-    if (warp == 0 && a.a_mode == TC_A_GATHER) {
+    if (warp == 0 && a.a_mode == TC_A_GATHER && a.ga_async) {
+        if (CG == 1) producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane);
+        __syncwarp();
+    } else if (warp == 0 && a.a_mode == TC_A_GATHER) {
         producer_gather<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units, lane);
         __syncwarp();
     } else if (warp == 0) {
@@ -1427,6 +1501,9 @@ static int pick_cg(int M) {
     if (forced == 1 || forced == 2) return forced;
     return M > BM ? 2 : 1;
 }
+// the cp.async gather producer fills single-CTA tiles (a lane's cp.async completion can only
+// arrive on its own CTA's barrier)
+static int pick_cg(const TcArgs& a) { return (a.a_mode == TC_A_GATHER && a.ga_async) ? 1 : pick_cg(a.M); }
 
 void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
@@ -1434,7 +1511,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.n2 != 2) a.n2 = 1;  // a re-configure (box64 rows) keeps the first call's choice
     if (a.block_n == 0) {
         a.n2 = 1;
-        const int cg = pick_cg(a.M);
+        const int cg = pick_cg(a);
         const long long m_units = (a.M + 128LL * cg - 1) / (128LL * cg);
         const int rows_real = a.M < 128 * cg ? a.M : 128 * cg;  // a lone short M tile loads no padding rows
         a.block_n = pick_block_n(a.Ncols, m_units, a.batch, num_sms / cg, cg, a.row_bytes, a.num_kb, rows_real);
@@ -1453,7 +1530,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     if (a.cm == CM_3XTF32 && a.block_n > 64) a.block_n = 64;  // register-resident fp32 partial sums
     // 3xTF32: promote the tensor-core partial sums to fp32 registers every 256 reduction elements
     a.promote_kb = a.cm == CM_3XTF32 ? (256 / (a.row_bytes / 4) > 0 ? 256 / (a.row_bytes / 4) : 1) : 0;
-    a.cg = pick_cg(a.M);
+    a.cg = pick_cg(a);
     a.epi_fast = knob("AI3_EPI_FAST", 1) != 0;
     a.trace = knob("AI3_TC_TRACE", 0) != 0;
     if (a.n2 == 2 && !a.epi_fast) a.n2 = 1;  // N sub-tiles run in the fast epilogue only
