@@ -19,42 +19,65 @@ constexpr int NT = 256;
 // filter column, one fmaf(w, x, acc) per tap, zero-padding taps included (x = 0) -- so both
 // kernels produce the same bits for every output (the choice depends on the batch size;
 // the result must not).
+// KS: compile-time square filter (0 = runtime R x S): the tap loops unroll, so every load of
+// an input channel's R*S taps is in flight before the first fmaf needs it (the kernel is
+// latency-bound: a handful of threads per SM, each a chain of C*R*S fmaf).
+template <int KS>
 __global__ void __launch_bounds__(NT) direct_small_kernel(const DirectArgs a) {
-    const int64_t total = a.N * a.K * a.P * a.Q;
+    const int R = KS ? KS : a.R, S = KS ? KS : a.S;
+    const uint32_t total = (uint32_t)(a.N * a.K * a.P * a.Q);  // < 2^31 (launch_direct)
+    const uint32_t K = (uint32_t)a.K, P = (uint32_t)a.P, Q = (uint32_t)a.Q;
     const int64_t xsN = a.in_nhwc ? a.H * a.W * a.C : a.C * a.H * a.W;
     const int64_t xsC = a.in_nhwc ? 1 : a.H * a.W;
     const int64_t xsH = a.in_nhwc ? a.W * a.C : a.W;
     const int64_t xsW = a.in_nhwc ? a.C : 1;
-    for (int64_t o = blockIdx.x * (int64_t)NT + threadIdx.x; o < total; o += (int64_t)gridDim.x * NT) {
-        int64_t n, k, p, q, t;
+    for (uint32_t o = blockIdx.x * NT + threadIdx.x; o < total; o += gridDim.x * NT) {
+        uint32_t n, k, p, q, t;
         if (a.out_nhwc) {  // k fastest: a warp's stores are contiguous
-            k = o % a.K; t = o / a.K; q = t % a.Q; t /= a.Q; p = t % a.P; n = t / a.P;
+            t = o / K; k = o - t * K; q = t % Q; t /= Q; p = t % P; n = t / P;
         } else {           // q fastest
-            q = o % a.Q; t = o / a.Q; p = t % a.P; t /= a.P; k = t % a.K; n = t / a.K;
+            t = o / Q; q = o - t * Q; p = t % P; t /= P; k = t % K; n = t / K;
         }
-        const int g = (int)(k / a.Kg), kk = (int)(k - (int64_t)g * a.Kg);
-        const int64_t xb = n * xsN + (int64_t)g * a.Cg * xsC;
-        const float* wg = a.w + (int64_t)g * a.Cg * a.R * a.S * a.Kgp + kk;
+        const int g = (int)(k / (uint32_t)a.Kg), kk = (int)(k - (uint32_t)g * a.Kg);
+        const int ih0 = (int)p * a.sh - a.ph, iw0 = (int)q * a.sw - a.pw;
+        const char* xb = reinterpret_cast<const char*>(a.x) + (n * xsN + (int64_t)g * a.Cg * xsC) * (a.bf16 ? 2 : 4);
+        const float* wg = a.w + (int64_t)g * a.Cg * R * S * a.Kgp + kk;
         float acc = 0.f;
         for (int c = 0; c < a.Cg; ++c) {
-            for (int r = 0; r < a.R; ++r) {
-                const int64_t ih = p * a.sh - a.ph + (int64_t)r * a.dh;
-                const bool row_ok = ih >= 0 && ih < a.H;
-                for (int s = 0; s < a.S; ++s) {
-                    const int64_t iw = q * a.sw - a.pw + (int64_t)s * a.dw;
-                    float xv = 0.f;
-                    if (row_ok && iw >= 0 && iw < a.W) {
-                        const int64_t i = xb + c * xsC + ih * xsH + iw * xsW;
-                        xv = a.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.x)[i])
-                                    : reinterpret_cast<const float*>(a.x)[i];
+            float xv[KS ? KS * KS : 1], wv[KS ? KS * KS : 1];
+            if (KS) {
+#pragma unroll
+                for (int r = 0; r < (KS ? KS : 1); ++r) {
+                    const int ih = ih0 + r * a.dh;
+#pragma unroll
+                    for (int sx = 0; sx < (KS ? KS : 1); ++sx) {
+                        const int iw = iw0 + sx * a.dw;
+                        const bool ok = (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+                        const int64_t i = c * xsC + ih * xsH + iw * xsW;
+                        xv[r * KS + sx] = !ok ? 0.f : (a.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xb)[i])
+                                                              : reinterpret_cast<const float*>(xb)[i]);
+                        wv[r * KS + sx] = __ldg(wg + (((int64_t)c * KS + r) * KS + sx) * a.Kgp);
                     }
-                    acc = fmaf(wg[(((int64_t)c * a.R + r) * a.S + s) * a.Kgp], xv, acc);
+                }
+#pragma unroll
+                for (int j = 0; j < (KS ? KS * KS : 1); ++j) acc = fmaf(wv[j], xv[j], acc);
+            } else {
+                for (int r = 0; r < R; ++r) {
+                    const int ih = ih0 + r * a.dh;
+                    for (int sx = 0; sx < S; ++sx) {
+                        const int iw = iw0 + sx * a.dw;
+                        const bool ok = (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
+                        const int64_t i = c * xsC + ih * xsH + iw * xsW;
+                        const float x1 = !ok ? 0.f : (a.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xb)[i])
+                                                             : reinterpret_cast<const float*>(xb)[i]);
+                        acc = fmaf(__ldg(wg + (((int64_t)c * R + r) * S + sx) * a.Kgp), x1, acc);
+                    }
                 }
             }
         }
         float v = acc + (a.bias ? a.bias[k] : 0.f);
         if (a.relu && v < 0.f) v = 0.f;
-        const int64_t oi = a.out_nhwc ? ((n * a.P + p) * a.Q + q) * a.K + k : ((n * a.K + k) * a.P + p) * a.Q + q;
+        const int64_t oi = a.out_nhwc ? (((int64_t)n * P + p) * Q + q) * K + k : (((int64_t)n * K + k) * P + p) * Q + q;
         if (a.bf16) reinterpret_cast<__nv_bfloat16*>(a.y)[oi] = __float2bfloat16_rn(v);
         else reinterpret_cast<float*>(a.y)[oi] = v;
     }
@@ -78,9 +101,14 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
         const long long ctas = ((a.P + tp - 1) / tp) * ((a.Q + tq - 1) / tq) * ((a.Kg + 8 * nkg - 1) / (8 * nkg)) *
                                a.N * a.G;
         const long long outs = a.N * a.K * a.P * a.Q;
-        if (ctas < device_num_sms() && (long long)a.Cg * a.R * a.S <= 4608) {
+        if (ctas < device_num_sms() && (long long)a.Cg * a.R * a.S <= 4608 && outs < (1LL << 31)) {
             const long long blocks = (outs + NT - 1) / NT;
-            direct_small_kernel<<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), NT, 0, st>>>(a);
+            const unsigned grid = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+            const bool sq = a.R == a.S;
+            if (sq && a.R == 3) direct_small_kernel<3><<<grid, NT, 0, st>>>(a);
+            else if (sq && a.R == 1) direct_small_kernel<1><<<grid, NT, 0, st>>>(a);
+            else if (sq && a.R == 5) direct_small_kernel<5><<<grid, NT, 0, st>>>(a);
+            else direct_small_kernel<0><<<grid, NT, 0, st>>>(a);
             return cudaGetLastError();
         }
     }
