@@ -10,6 +10,9 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402
+if len(sys.argv) > 1 and sys.argv[1] == "--dev":  # developer build (knobs such as AI3_TC_CG=1)
+    from paper_2410_08300_b200 import _lib  # noqa: E402
+    _lib.select_library(os.path.join(ROOT, "paper_2410_08300_b200", "libai3_dev.so"))
 import paper_2410_08300_b200 as ai3  # noqa: E402
 from paper_2410_08300_b200 import layers as L  # noqa: E402
 from synth import CONFIG1, ConvShape, conv_inputs  # noqa: E402
