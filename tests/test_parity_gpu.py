@@ -177,6 +177,22 @@ def test_deterministic_and_batch_independent(algo):
         assert torch.equal(part, y1[s:s + 2])
 
 
+@pytest.mark.parametrize("dtype,layout", [("f32", "nchw"), ("bf16", "nhwc")])
+def test_direct_small_and_tiled_kernels_agree_bitwise(dtype, layout):
+    """`direct` runs a one-thread-per-output kernel when the layer has fewer tiles than SMs
+    (here at N = 1) and the tiled kernel otherwise (N = 96): both reduce in the same fmaf
+    order, so image 0 comes out with the same bits either way (batch-size independence)."""
+    import paper_2410_08300_b200 as ai3
+    shape = ConvShape("smallvtiled", 96, 16, 32, 32, 32, 3, 3, 1, 1)
+    x, w, b = inputs(shape, 5, dtype)
+    xt, wt, bt = to_device(x, dtype, layout), to_device(w, dtype), to_device(b, dtype)
+    big = ai3.conv2d(xt, wt, bt, 1, 1, 1, 1, "direct")
+    one = ai3.conv2d(to_device(x[:1], dtype, layout), wt, bt, 1, 1, 1, 1, "direct")
+    assert torch.equal(one, big[:1])
+    ref = oracle.conv2d(x[:1], w, b, 1, 1, 1, 1)
+    assert oracle.rel_err(one.double().cpu().numpy(), ref) <= (1e-5 if dtype == "f32" else 2e-2)
+
+
 # (the harness has teeth, SPEC.md:572: tests/test_mutation_gpu.py runs it against a faulty build)
 
 
