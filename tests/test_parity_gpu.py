@@ -30,6 +30,19 @@ def _supports(shape: ConvShape, algo: str) -> bool:
     return True
 
 
+def _expect_unsupported(shape, algo):
+    """An algorithm whose preconditions the layer violates (Winograd off 3x3 / stride 1,
+    tensor-core algorithms with groups, R5) must say so -- supported() is False and a call
+    raises UnsupportedConfiguration -- instead of computing anything."""
+    import paper_2410_08300_b200 as ai3
+    x, w, b = inputs(shape, 1, "f32")
+    xt, wt = to_device(x, "f32"), to_device(w, "f32")
+    assert not ai3.supported(xt.shape, shape.K, (shape.R, shape.S), shape.stride, shape.pad, shape.dil, shape.groups,
+                             torch.float32, algorithm=algo)
+    with pytest.raises(ai3.UnsupportedConfiguration):
+        ai3.conv2d(xt, wt, None, shape.stride, shape.pad, shape.dil, shape.groups, algo)
+
+
 def _check(shape, algo, dtype, math, layout, seed, plan=True):
     x, w, b = inputs(shape, seed, dtype)
     y = run_ai3(shape, x, w, b, algo, dtype, math, layout, plan)
@@ -76,7 +89,7 @@ RAGGED = [
 @pytest.mark.parametrize("dtype,math", MODES)
 def test_ragged_shapes(shape, algo, dtype, math):
     if not _supports(shape, algo):
-        pytest.skip("algorithm precondition")
+        return _expect_unsupported(shape, algo)
     _check(shape, algo, dtype, math, "nhwc" if shape.C % 2 == 0 else "nchw", seed=stable_seed(shape.name))
 
 
@@ -110,7 +123,7 @@ def _sweep(count, seed):
 @pytest.mark.parametrize("algo", ALGOS)
 def test_spec_sweep(shape, algo):
     if not _supports(shape, algo):
-        pytest.skip("algorithm precondition")
+        return _expect_unsupported(shape, algo)
     for dtype, math in (("f32", "strict"), ("bf16", "strict")):
         _check(shape, algo, dtype, math, "nchw", seed=stable_seed((shape.name, algo)))
 
@@ -128,7 +141,7 @@ def test_integer_inputs_bit_exact(shape, algo, dtype, math):
     operand exact in tf32 / bf16), so each path must reproduce the oracle bit for bit.
     bf16 outputs additionally need |y| <= 256: use x, w in {-1, 0, 1} there."""
     if not _supports(shape, algo):
-        pytest.skip("algorithm precondition")
+        return _expect_unsupported(shape, algo)
     small = dtype == "bf16"
     x, w, b = integer_inputs(shape, seed=5, xmax=1 if small else 8, wmax=1 if small else 4)
     if small and shape.C * shape.R * shape.S > 250:
@@ -154,7 +167,7 @@ DEGEN = [ConvShape("out1x1", 2, 8, 3, 3, 5, 3, 3), ConvShape("k1", 1, 4, 6, 6, 1
 @pytest.mark.parametrize("algo", ALGOS)
 def test_degenerate(shape, algo):
     if not _supports(shape, algo):
-        pytest.skip("algorithm precondition")
+        return _expect_unsupported(shape, algo)
     _check(shape, algo, "f32", "strict", "nchw", seed=3)
     _check(shape, algo, "bf16", "strict", "nhwc", seed=4)
 
