@@ -185,36 +185,44 @@ def run_launch_check(rank: int, world: int):
 
 
 # ---------------------------------------------------------------------------- oracle legs
-def _oracle_run(layers, k: int, seed: int = 7):
-    """The fp64 oracle on one image of every layer, first k output channels (a bounded
-    sample of the step: conv is independent per output channel).  Returns (flops, secs)."""
+def _oracle_run(layers, k: int, seed: int = 7, images: int = 1):
+    """The fp64 oracle on `images` images of every layer, first k output channels (a bounded
+    sample of the step: conv is independent per image and per output channel).
+    Returns (flops, secs)."""
     import oracle
     threads = oracle.host_threads()
     flops, secs = 0, 0.0
     for i, l in enumerate(layers):
-        x, w, b = conv_inputs(l.with_batch(1), seed + i, "bf16")
+        x, w, b = conv_inputs(l.with_batch(images), seed + i, "bf16")
         kk = min(k, l.K)
         t0 = time.perf_counter()
         oracle.conv2d(x, w[:kk], b[:kk], l.stride, l.pad, l.dil, l.groups, threads=threads)
         secs += time.perf_counter() - t0
-        flops += 2 * kk * (l.C // l.groups) * l.R * l.S * l.P * l.Q
+        flops += 2 * images * kk * (l.C // l.groups) * l.R * l.S * l.P * l.Q
     return flops, secs
 
 
 def _oracle_calibrate(layers, seconds: float):
-    """Smallest k (output channels per layer) whose sample takes >= `seconds`."""
+    """Smallest sample (k output channels per layer, then whole images) taking >= `seconds`:
+    returns (k, images)."""
     import oracle
     oracle.build()
-    k = 1
+    kmax = max(l.K for l in layers)
+    k, images = 1, 1
     while True:
-        _, dt = _oracle_run(layers, k)
-        if dt >= seconds or k >= 64:
-            return k
-        k = min(64, max(k + 1, int(k * min(8.0, 1.2 * seconds / max(dt, 1e-3)))))
+        _, dt = _oracle_run(layers, k, images=images)
+        if dt >= seconds or images >= 64:
+            return k, images
+        grow = min(8.0, 1.2 * seconds / max(dt, 1e-3))
+        if k < kmax:
+            k = min(kmax, max(k + 1, int(k * grow)))
+        else:
+            images = min(64, max(images + 1, int(images * grow)))
 
 
-def _sample_desc(layers, k: int, flops: int, threads: int) -> str:
-    return (f"1 image x first {k} output channel(s) of each of the {len(layers)} {WORKLOAD} layers "
+def _sample_desc(layers, k: int, flops: int, threads: int, images: int = 1) -> str:
+    ch = "every output channel" if k >= max(l.K for l in layers) else f"first {k} output channel(s)"
+    return (f"{images} image(s) x {ch} of each of the {len(layers)} {WORKLOAD} layers "
             f"({flops / 1e9:.2f} GFLOP), fp64 oracle, {threads} threads")
 
 
@@ -225,15 +233,15 @@ def run_reference(args, rank: int, world: int):
     import oracle
     layers = workload("vgg16", BATCH)
     per_step = max(0.5, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
-    k = _oracle_calibrate(layers, per_step)
+    k, images = _oracle_calibrate(layers, per_step)
     times, flops = [], 0
     for i in range(args.warmup + args.steps):
-        flops, dt = _oracle_run(layers, k)
+        flops, dt = _oracle_run(layers, k, images=images)
         if i >= args.warmup:
             times.append(dt)
     mean = sum(times) / len(times)
     value = flops / mean / 1e12
-    desc = _sample_desc(layers, k, flops, oracle.host_threads())
+    desc = _sample_desc(layers, k, flops, oracle.host_threads(), images)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -671,10 +679,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     cpu = None
     if world == 1 and not args.no_cpu:  # the oracle on host cores (rank 0, N=1 only)
         import oracle
-        k = _oracle_calibrate(specs, args.cpu_seconds)
-        flops, dt = _oracle_run(specs, k)
+        k, images = _oracle_calibrate(specs, args.cpu_seconds)
+        flops, dt = _oracle_run(specs, k, images=images)
         cpu = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.host_threads(), "kind": "oracle",
-               "sample": _sample_desc(specs, k, flops, oracle.host_threads()), "seconds": round(dt, 2)}
+               "sample": _sample_desc(specs, k, flops, oracle.host_threads(), images), "seconds": round(dt, 2)}
 
     if dist:
         dist.barrier()  # every rank stays until rank 0's extra legs are done
