@@ -390,6 +390,13 @@ __device__ __forceinline__ float4 lds128f(uint32_t saddr) {
                  : "memory");
     return v;
 }
+// *dst += v, element-wise, performed at L2 (fire-and-forget: no load-to-use latency in the
+// issuing thread).  Deterministic as long as no element receives two reductions within one
+// kernel (the caller's contract), since then every element sees its adds in launch order.
+__device__ __forceinline__ void red_add_v4(float* dst, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 }  // namespace ai3
 
 // ================================================================== 4-D tiled TMA + halo descriptors

@@ -162,13 +162,9 @@ __device__ __forceinline__ void kn2row_store(const TcArgs& a, const float (&f)[3
 #pragma unroll
             for (int j = 0; j < 8; ++j) d4[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
         } else {
-            float4 old[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) old[j] = d4[j];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                d4[j] = make_float4(old[j].x + f[4 * j], old[j].y + f[4 * j + 1], old[j].z + f[4 * j + 2],
-                                    old[j].w + f[4 * j + 3]);
+                red_add_v4(reinterpret_cast<float*>(d4 + j), make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]));
         }
     } else {
 #pragma unroll
@@ -1257,12 +1253,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const float4 v = *reinterpret_cast<const float4*>(&u);
                         float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (int64_t)t * a.Ncols +
                                                                 col0) + qd;
-                        if (a.kn == 2) {
-                            *dst = v;
-                        } else {
-                            const float4 o = *dst;
-                            *dst = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
-                        }
+                        if (a.kn == 2) *dst = v;
+                        else red_add_v4(reinterpret_cast<float*>(dst), v);
                     }
                 }
                 return;
