@@ -287,6 +287,7 @@ struct ai3_plan {
     int ksplit = 1;           // split-K factor (linear-like plans): partials in ws_M, reduced into y
     bool kn_inplace = false;  // kn2row: fp32 NHWC output accumulates in y itself (no workspace)
     int kn_first = -1;        // kn2row: a tap covering every output pixel (runs first, writes), or -1
+    bool wf = false;          // winograd: fused output transform in the GEMM epilogue (no M, TcArgs::wf)
 };
 
 namespace {
@@ -506,11 +507,23 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
         pl.ws_Vlo = ws;
         if (pl.splits == 2) ws = align_up(ws + (size_t)16 * T * pl.Cpad * e);
-        // M in bf16 for bf16 runs (halves the dominant M write + read: the transformed-domain
-        // products are rounded once more, R26), fp32 otherwise
+        // bf16 NHWC outputs with K <= 64: the fused kernel (TcArgs::wf) keeps M in TMEM and
+        // writes y from the GEMM epilogue.  Its 16 accumulators fill TMEM at 32 columns each, so
+        // every T tile of V is re-read from L2 once per 32 output channels; measured (DESIGN.md
+        // §6), that wins only while K / 32 <= 2 (VGG conv1_2 1396 -> 1156 us, conv3_2 365 -> 553
+        // us).  Otherwise M goes to the workspace -- bf16 for bf16 runs (halves the M write +
+        // read: the transformed-domain products are rounded once more, R26), fp32
+        // otherwise -- and an output-transform pass follows.
+        pl.wf = pl.cm == CM_BF16 && c.out_layout == AI3_NHWC && c.K % 16 == 0 &&
+                c.K <= knob("AI3_WINO_FUSED_KMAX", 64) && knob("AI3_WINO_FUSED", 1) != 0;
         const size_t m_elem = pl.cm == CM_BF16 ? 2 : 4;
         pl.ws_M = ws;
-        ws = align_up(ws + (size_t)16 * T * c.K * m_elem);
+        if (!pl.wf) ws = align_up(ws + (size_t)16 * T * c.K * m_elem);
+        a.wf = pl.wf ? 1 : 0;
+        a.wf_P = (int)c.P;
+        a.wf_Q = (int)c.Q;
+        a.wf_TH = (int)((c.P + 1) / 2);
+        a.wf_TW = (int)((c.Q + 1) / 2);
         a.a_mode = TC_A_TILED3D;
         a.M = (int)T;
         a.batch = 16;
@@ -519,7 +532,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.out_bf16 = pl.cm == CM_BF16 ? 1 : 0;  // M's element type
         a.epi_PQ = (int)T;     // [16][K][T] when the final output is NCHW
         a.out_bstride = (long long)T * c.K;
-        pl.launches = (pl.need_prep ? 1 : 0) + 3;
+        pl.launches = (pl.need_prep ? 1 : 0) + (pl.wf ? 2 : 3);
     }
     // split-K for linear-like plans (a 1x1 output map: nn.Linear, flatten -> linear): S K-ranges
     // whose fp32 partials a reduce pass sums (splitk.cu).  S depends on N and K only -- never on
@@ -670,8 +683,10 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         oka = encode_tiled(&pl.ta0, dt, 2, src, dims, str, box, sw);
         if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 2, src_lo, dims, str, box, sw);
     } else {
+        // V[16][T][Cpad], or tile-major V[T][16][Cpad] for the fused kernel (its CTAs read all 16
+        // components of one T tile back to back: one tile's rows stay within a few pages)
         const uint64_t dims[3] = {(uint64_t)pl.Cpad, (uint64_t)a.M, 16};
-        const uint64_t str[2] = {pl.Cpad * e, (uint64_t)a.M * pl.Cpad * e};
+        const uint64_t str[2] = {(pl.wf ? 16 : 1) * pl.Cpad * e, (pl.wf ? 1 : (uint64_t)a.M) * pl.Cpad * e};
         const uint32_t box[3] = {kel, 128, 1};
         oka = encode_tiled(&pl.ta0, dt, 3, src, dims, str, box, sw);
         if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 3, src_lo, dims, str, box, sw);
@@ -857,12 +872,16 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.out = y;
     } else {
         e = launch_winograd_input(xs, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, c.ph, c.pw, pl.cm, nullptr, w + pl.ws_V,
-                                  w + pl.ws_Vlo, st);
+                                  w + pl.ws_Vlo, pl.wf ? 1 : 0, st);
         if (e != cudaSuccess) return cuda_fail(e, "winograd input transform launch");
         if ((s = encode_a_maps(pl, w + pl.ws_V, w + pl.ws_Vlo)) != AI3_OK) return s;
-        tp.args.out = w + pl.ws_M;
-        tp.args.bias = nullptr;
-        tp.args.relu = 0;
+        if (pl.wf) {
+            tp.args.out = y;  // bias, ReLU applied by the fused output transform
+        } else {
+            tp.args.out = w + pl.ws_M;
+            tp.args.bias = nullptr;
+            tp.args.relu = 0;
+        }
     }
     if (tp.args.stg_row && !aligned(tp.args.out, 16)) {  // TMA stores need a 16-byte base
         if (tp.args.n2 == 2 || tp.args.pool)  // these run only with the TMA-store epilogue
@@ -879,7 +898,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
                                  c.dtype == AI3_BF16, pl.relu, st);
         if (e != cudaSuccess) return cuda_fail(e, "split-K reduce launch");
     }
-    if (pl.algo == AI3_ALGO_WINOGRAD) {
+    if (pl.algo == AI3_ALGO_WINOGRAD && !pl.wf) {
         e = launch_winograd_output(w + pl.ws_M, tp.args.out_bf16, tp.args.out_nchw, bias, y, c.out_layout == AI3_NHWC,
                                    c.dtype == AI3_BF16, c.N, c.K, c.P, c.Q, pl.relu, st);
         if (e != cudaSuccess) return cuda_fail(e, "winograd output transform launch");

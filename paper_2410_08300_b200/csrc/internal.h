@@ -143,10 +143,11 @@ cudaError_t launch_pack_weights_taps(const void* w, ai3_dtype dtype, int64_t K, 
 // KCRS weights -> [K][Kp] with columns (r, s, c) over the exact R*S*C (zero tail), compute mode (+ lo).
 cudaError_t launch_pack_weights_flat(const void* w, ai3_dtype dtype, int64_t K, int64_t C, int64_t R, int64_t S,
                                      int64_t Kp, ComputeMode cm, void* dst, void* dst_lo, cudaStream_t st);
-// NHWC (Cpad) -> V[16][T][Cpad], T = N*ceil(P/2)*ceil(Q/2), rounded per compute mode (+ lo).
+// NHWC (Cpad) -> V[16][T][Cpad] (tmajor: V[T][16][Cpad]), T = N*ceil(P/2)*ceil(Q/2), rounded
+// per compute mode (+ lo).
 cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P,
                                   int64_t Q, int ph, int pw, ComputeMode cm, const void* x_lo, void* V, void* V_lo,
-                                  cudaStream_t st);
+                                  int tmajor, cudaStream_t st);
 // M (fp32, or bf16 if m_bf16; [16][K][T] if out NCHW else [16][T][K]) -> y (+bias), cropped to P x Q.
 cudaError_t launch_winograd_output(const void* M, int m_bf16, int m_kt, const float* bias, void* y, int out_nhwc, int bf16,
                                    int64_t N, int64_t K, int64_t P, int64_t Q, int relu, cudaStream_t st);
@@ -220,6 +221,12 @@ struct TcArgs {
     int ga_pitch;
     const char* ga_src;
     const char* ga_src_lo;
+    // fused Winograd F(2x2,3x3) (wf = 1; batch = 16, block_n = 32, bf16): every CTA group runs
+    // the 16 transformed-domain GEMMs of one (T tile, 32-channel) unit back to back, one TMEM
+    // accumulator per component xi*4+nu (16 x 32 = 512 columns), and the epilogue applies the
+    // output transform Y = A^T M A (+ bias, ReLU) straight from TMEM into the NHWC bf16 output
+    // `out` (N, wf_P, wf_Q, Ncols); T = N * wf_TH * wf_TW tiles of 2 x 2 output pixels.  No M.
+    int wf, wf_P, wf_Q, wf_TH, wf_TW;
     const float* bias;  // fp32 [Ncols] or null
     void* out;
     long long out_bstride;  // elements between batches

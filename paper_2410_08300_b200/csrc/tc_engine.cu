@@ -39,8 +39,13 @@ namespace {
 constexpr int BM = 128;
 constexpr int NUM_EPI_WARPS = 8;    // two epilogue warpgroups, alternating tiles
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
+// implicit_precomp_gemm's cp.async gather: NUM_GA_EXTRA more producer warps (warps 10, 11)
+// share each A tile's rows with warp 0 -- one warp's address / cp.async issue chain was the
+// limit; the other modes launch NUM_THREADS
+constexpr int NUM_GA_EXTRA = 2;
+constexpr int NUM_THREADS_GA = NUM_THREADS + 32 * NUM_GA_EXTRA;
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
-constexpr int MAX_ACC = 8;          // TMEM accumulator buffers (n_acc * block_n <= 512 columns)
+constexpr int MAX_ACC = 16;         // TMEM accumulator buffers (n_acc * block_n <= 512 columns; > 8 only for wf)
 }  // namespace
 
 
@@ -173,6 +178,28 @@ __device__ __forceinline__ void kn2row_store(const TcArgs& a, const float (&f)[3
     }
 }
 
+// Tile walk of one CTA group.  Default: tiles unit, unit + num_units, ... of the (batch, M
+// tile, N tile) order, batch outermost.  Fused Winograd (a.wf): the group takes the (M, N)
+// units unit, unit + num_units, ... and runs the 16 batches (transform components) of each
+// back to back, so that its 16 accumulators sit in TMEM together for the output transform.
+__device__ __forceinline__ int unit_tiles(const TcArgs& a, int unit, int num_units) {
+    const int tpb = a.m_tiles * a.n_tiles;
+    const int total = a.wf ? tpb : tpb * a.batch;
+    const int mine = unit < total ? (total - unit + num_units - 1) / num_units : 0;
+    return a.wf ? 16 * mine : mine;
+}
+__device__ __forceinline__ void tile_at(const TcArgs& a, int unit, int num_units, int j, int& b, int& rem) {
+    const int tpb = a.m_tiles * a.n_tiles;
+    if (a.wf) {
+        b = j & 15;
+        rem = unit + (j >> 4) * num_units;
+    } else {
+        const int tile = unit + j * num_units;
+        b = tile / tpb;
+        rem = tile - b * tpb;
+    }
+}
+
 // ---------------------------------------------------------------- TMA producer (one thread)
 // Walks the K-blocks of every tile of this CTA group and streams A/B tiles into the smem
 // ring.  Filter-tap / channel-chunk coordinates advance incrementally (no division in
@@ -192,9 +219,11 @@ __device__ __forceinline__ void producer(const TcArgs& a, const CUtensorMap& ta0
     const uint32_t full_base = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = unit; tile < total_tiles; tile += num_units) {
-        const int b = tile / tiles_per_batch;
-        const int rem = tile - b * tiles_per_batch;
+    const int my_tiles = unit_tiles(a, unit, num_units);
+    for (int j = 0; j < my_tiles; ++j) {
+        const int tile = unit + j * num_units;  // (batch-outermost order; L2 prefetch only)
+        int b, rem;
+        tile_at(a, unit, num_units, j, b, rem);
         const int mt = rem / a.n_tiles;
         const int m0 = mt * (BM * CG) + (int)rank * BM;
         const int n0 = (rem - mt * a.n_tiles) * a.block_n * a.n2 + (int)rank * bn_cta;
@@ -377,9 +406,13 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
 // generic -> async proxy after acquiring the barrier (the tensor core reads smem through the
 // async proxy).  (Measured: one TMA gather4 per 4 rows issued ~1 per 87 cycles per SM, so the
 // gather4 producer ran VGG conv3_2 at 0.13 of the tensor rate.)
+// pid: this producer warp's index (0 .. NUM_GA_EXTRA); it copies the 4-row groups
+// [j0, j1) of every A tile, and warp 0 also issues the B tile's TMA load.
 __device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUtensorMap& tb0, const CUtensorMap& tb1,
                                                       uint8_t* smem, uint64_t* full, uint64_t* empty, int unit,
-                                                      int num_units, int lane) {
+                                                      int num_units, int lane, int pid) {
+    constexpr int NP = 1 + NUM_GA_EXTRA;
+    const int j0 = pid * 32 / NP, j1 = (pid + 1) * 32 / NP;
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
     const uint32_t a_bytes = BM * 128u, b_bytes = (uint32_t)a.block_n * 128u;
     const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
@@ -409,16 +442,19 @@ __device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUt
             }
             if (lane == 0) {
                 mbar_wait(&empty[stage], phase ^ 1);
-                mbar_arrive_expect_tx(&full[stage], splits * b_bytes);
-                uint8_t* sB = smem + stage * stage_bytes + splits * a_bytes;
-                tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
-                if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
+                if (pid == 0) {
+                    mbar_arrive_expect_tx(&full[stage], splits * b_bytes);
+                    uint8_t* sB = smem + stage * stage_bytes + splits * a_bytes;
+                    tma_load_2d(sB, &tb0, &full[stage], kb * kelems, n0);
+                    if (splits == 2) tma_load_2d(sB + b_bytes, &tb1, &full[stage], kb * kelems, n0);
+                }
             }
             __syncwarp();
             const uint32_t sA = s0 + stage * stage_bytes;
             const size_t col = (size_t)cc * 128 + chunk * 16;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3; this lane: row 4j + sub_row, chunk
+                if (j < j0 || j >= j1) continue;
                 const int row = 4 * j + sub_row;
                 const int reg = row >> 5;
                 const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
@@ -454,12 +490,12 @@ __device__ __forceinline__ void mma_issuer(const TcArgs& a, uint8_t* smem, uint6
     const uint64_t a_desc0 = make_sdesc(s0, a.row_bytes);
     const uint64_t b_desc0 = make_sdesc(s0 + splits * a_bytes, a.row_bytes);
     const uint64_t alo_off = a_bytes >> 4, blo_off = b_bytes >> 4;
-    const int tiles = a.m_tiles * a.n_tiles * a.batch;
+    const int my_tiles = unit_tiles(a, unit, num_units);
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
     int stage = 0, acc = 0, kc = 0;
     uint32_t phase = 0, acc_phase = 0;
     uint32_t d_tmem = tmem_base;
-    for (int tile = unit; tile < tiles; tile += num_units) {
+    for (int j = 0; j < my_tiles; ++j) {
         kc = 0;
         for (int kb = 0; kb < a.num_kb; ++kb) {
             if (kc == 0) {
@@ -1041,12 +1077,118 @@ __device__ __forceinline__ void epilogue_fast(const TcArgs& a, const CUtensorMap
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- fused Winograd epilogue (a.wf)
+// Output transform of F(2x2,3x3) straight from TMEM (§V.B(d); SURVEY §8 row a8
+// step (iv)): Y = A^T M A, A^T = [[1,1,1,0],[0,1,-1,-1]], + bias (fp32), ReLU, bf16 NHWC.
+// Both epilogue warpgroups drain every unit: warpgroup g owns columns 16g..16g+15 of the
+// 32-column accumulators; TMEM lane = the warp's quarter row = transform tile t.  The 16
+// accumulators (component xi*4+nu in buffer xi*4+nu) are read one row xi at a time and
+// released right after the read, so the next unit's GEMMs start on them while this unit's
+// transform finishes.  Per row xi: s[c] = sum_nu M[xi][nu] A[nu][c] (M A), then
+// Y[r][c] += A^T[r][xi] s[c].
+template <int CG>
+__device__ __forceinline__ void epilogue_wino(const TcArgs& a, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                              uint32_t rank, int unit, int num_units, int warp, int lane) {
+    const int quarter = warp & 3;
+    const int g = (warp - 2) >> 2;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+    const int groups = unit_tiles(a, unit, num_units) >> 4;
+    const int thw = a.wf_TH * a.wf_TW;
+    const unsigned long long t_epi0 = TRACE_CLOCK(a);
+    for (int gi = 0; gi < groups; ++gi) {
+        const uint32_t ph = (uint32_t)(gi & 1);
+        const int rem = unit + gi * num_units;
+        const int mt = rem / a.n_tiles;
+        const int col0 = (rem - mt * a.n_tiles) * 32 + 16 * g;
+        const int t = mt * (BM * CG) + (int)rank * BM + quarter * 32 + lane;
+        float y[2][2][16];
+#pragma unroll
+        for (int xi = 0; xi < 4; ++xi) {
+            uint32_t v[4][16];
+#pragma unroll
+            EPI_TRACE(5, {
+                for (int nu = 0; nu < 4; ++nu) mbar_wait(&tfull[xi * 4 + nu], ph);
+            });
+            tc_fence_after();
+#pragma unroll
+            for (int nu = 0; nu < 4; ++nu)
+                tmem_ld16(tmem_base + lane_off + (uint32_t)((xi * 4 + nu) * 32 + 16 * g), v[nu]);
+            EPI_TRACE(8, tmem_ld_wait());
+#pragma unroll
+            for (int nu = 0; nu < 4; ++nu) tmem_regs_after_wait16(v[nu]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int nu = 0; nu < 4; ++nu) {
+                    if (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + (xi * 4 + nu) * 8);
+                    else mbar_arrive_relaxed(&tempty[xi * 4 + nu]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float m0 = __uint_as_float(v[0][j]), m1 = __uint_as_float(v[1][j]);
+                const float m2 = __uint_as_float(v[2][j]), m3 = __uint_as_float(v[3][j]);
+                const float s0 = m0 + m1 + m2, s1 = m1 - m2 - m3;
+                if (xi == 0) { y[0][0][j] = s0; y[0][1][j] = s1; }
+                else if (xi == 1) { y[0][0][j] += s0; y[0][1][j] += s1; y[1][0][j] = s0; y[1][1][j] = s1; }
+                else if (xi == 2) { y[0][0][j] += s0; y[0][1][j] += s1; y[1][0][j] -= s0; y[1][1][j] -= s1; }
+                else { y[1][0][j] -= s0; y[1][1][j] -= s1; }
+            }
+        }
+        if (t >= a.M || col0 >= a.Ncols) continue;
+        if (a.bias) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+                const float4 bv = *reinterpret_cast<const float4*>(a.bias + col0 + j);
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        y[r][c][j] += bv.x; y[r][c][j + 1] += bv.y; y[r][c][j + 2] += bv.z; y[r][c][j + 3] += bv.w;
+                    }
+            }
+        }
+        const int n = t / thw, rt = t - n * thw;
+        const int ty = rt / a.wf_TW, tx = rt - ty * a.wf_TW;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int p = 2 * ty + r;
+            if (p >= a.wf_P) break;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int q = 2 * tx + c;
+                if (q >= a.wf_Q) break;
+                __align__(16) __nv_bfloat162 h[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    float lo = y[r][c][2 * e], hi = y[r][c][2 * e + 1];
+                    if (a.relu) { lo = lo < 0.f ? 0.f : lo; hi = hi < 0.f ? 0.f : hi; }  // NaN passes (torch.relu)
+                    h[e] = __floats2bfloat162_rn(lo, hi);
+                }
+                __nv_bfloat16* dst =
+                    reinterpret_cast<__nv_bfloat16*>(a.out) + (((int64_t)n * a.wf_P + p) * a.wf_Q + q) * a.Ncols + col0;
+                if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(h)[0];
+                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(h)[1];
+                } else {  // a caller's misaligned output view
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) { dst[2 * e] = h[e].x; dst[2 * e + 1] = h[e].y; }
+                }
+            }
+        }
+    }
+    EPI_TRACE_ADD(6, t_epi0);
+    if (TRACE_ON(a) && warp == 2 && lane == 0) g_tc_trace[blockIdx.x][7] += groups;
+}
+
 // CG = CTAs per MMA: 1, or 2 (a CTA pair in a cluster issuing tcgen05.mma.cta_group::2:
 // the pair computes a 256 x BLOCK_N tile, each CTA loading its own 128 A rows and half
 // of the B rows, which halves the L2->SM operand traffic per FLOP -- the binding limit
 // of the 1-CTA kernel).
 template <int CG>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS_GA, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta0, const __grid_constant__ CUtensorMap ta1,
                    const __grid_constant__ CUtensorMap tb0, const __grid_constant__ CUtensorMap tb1,
                    const __grid_constant__ CUtensorMap tout, const TcArgs a, const int tmem_cols) {
@@ -1069,10 +1211,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_prefetch_desc(&tb0);
         if (splits == 2) { tma_prefetch_desc(&ta1); tma_prefetch_desc(&tb1); }
         // cp.async gather: B's transaction bytes + one arrival per CTA's A rows
-        const uint32_t full_count = (a.a_mode == TC_A_GATHER && a.ga_async) ? 1 + 32 : 1;
+        const uint32_t full_count = (a.a_mode == TC_A_GATHER && a.ga_async) ? 1 + 32 * (1 + NUM_GA_EXTRA) : 1;
         for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], full_count); mbar_init(&empty[s], 1); }
         // n2 == 2: both epilogue warpgroups drain every accumulator (one N sub-tile each)
-        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG * a.n2); }
+        // (fused Winograd: both warpgroups drain every accumulator, 16 columns each)
+        for (int i = 0; i < a.n_acc; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4 * CG * a.n2 * (a.wf ? 2 : 1)); }
         mbar_init(bres, 1);
         fence_mbar_init();
     }
@@ -1097,7 +1240,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
     if (warp == 0 && a.a_mode == TC_A_GATHER && a.ga_async) {
-        if (CG == 1) producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane);
+        if (CG == 1) producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane, 0);
+        __syncwarp();
+    } else if (warp >= 2 + NUM_EPI_WARPS) {  // extra gather producers (launched for ga_async only)
+        if (CG == 1 && a.a_mode == TC_A_GATHER && a.ga_async)
+            producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane, warp - (1 + NUM_EPI_WARPS));
         __syncwarp();
     } else if (warp == 0 && a.a_mode == TC_A_GATHER) {
         producer_gather<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units, lane);
@@ -1142,6 +1289,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (TRACE_ON(a) && leader && elected) g_tc_trace[blockIdx.x][4] += clock64() - t_mma0;
         __syncwarp();
+    } else if (a.wf) {
+        epilogue_wino<CG>(a, tfull, tempty, tmem_base, rank, unit, num_units, warp, lane);
     } else {
         const unsigned long long t_epi0 = TRACE_CLOCK(a);
         // ------------------------------------------------------------ epilogue (warps 2..5)
@@ -1499,6 +1648,13 @@ static int pick_cg(const TcArgs& a) { return (a.a_mode == TC_A_GATHER && a.ga_as
 
 void tc_configure(TcPlan& p, int num_sms) {
     TcArgs& a = p.args;
+    if (a.wf) {  // fused Winograd: 16 accumulators of 32 columns fill TMEM (see TcArgs::wf)
+        a.block_n = 32;
+        a.n2 = 1;
+        a.stg_row = 0;
+        a.box64 = 0;
+        a.bias_smem = 0;
+    }
     if (a.block_n == 0 && a.a_mode != TC_A_HALO) a.block_n = knob("AI3_BN", 0);  // dev override: force BLOCK_N
     if (a.n2 != 2) a.n2 = 1;  // a re-configure (box64 rows) keeps the first call's choice
     if (a.block_n == 0) {
@@ -1545,7 +1701,10 @@ void tc_configure(TcPlan& p, int num_sms) {
     // epilogue staging buffers per warp: deeper when the operand ring does not need the room
     auto stages_for = [&](int nstg) {
         int st = (SMEM_LIMIT - fixed - NUM_EPI_WARPS * nstg * 32 * a.stg_row) / stage_bytes;
-        return st > 8 ? 8 : st;
+        // fused Winograd: a unit streams 16 stages (one per component), so the ring must hold
+        // more than one unit's worth of small stages to cover the load latency (conv1_1: 2 KB)
+        const int cap = a.wf ? 32 : 8;
+        return st > cap ? cap : st;
     };
     const int base_stages = stages_for(2);
     a.n_stg = 2;
@@ -1585,7 +1744,7 @@ void tc_configure(TcPlan& p, int num_sms) {
     // as many TMEM accumulator buffers as fit (short-K tiles let the MMA run several tiles ahead
     // of the epilogue); 3xTF32 keeps 2 (it already chunks the K loop)
     a.n_acc = 512 / (a.block_n * a.n2);
-    if (a.n_acc > MAX_ACC) a.n_acc = MAX_ACC;
+    if (a.n_acc > (a.wf ? MAX_ACC : 8)) a.n_acc = a.wf ? MAX_ACC : 8;
     if (a.cm == CM_3XTF32) {
         // 3xTF32: `nch` accumulation chunks per tile; 2 x nch buffers let the two epilogue
         // warpgroups alternate tiles on disjoint buffers, else one warpgroup drains them all
@@ -1640,7 +1799,7 @@ cudaError_t launch_tc(const TcPlan& p, const CUtensorMap* a0, const CUtensorMap*
     // waits (griddepcontrol.wait) for that kernel's completion before any global access
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.blockDim = dim3(p.args.a_mode == TC_A_GATHER && p.args.ga_async ? NUM_THREADS_GA : NUM_THREADS);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];

@@ -350,12 +350,12 @@ __device__ __forceinline__ float bt_comb(const float (&r)[4], int a) {
 template <bool BF16IN, typename IDX>
 __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restrict__ xin, int N, int H, int W, int Cpad,
                                                              int TH, int TW, int ph, int pw, int cm, void* V,
-                                                             void* V_lo) {
+                                                             void* V_lo, int tmajor) {
     constexpr int VC = 4;
     const IDX groups = (IDX)(Cpad / VC);
     const int64_t T = (int64_t)N * TH * TW;
     const IDX total = (IDX)(T * groups);
-    const int64_t plane = T * Cpad;  // elements between V planes
+    const int64_t plane = tmajor ? Cpad : T * Cpad;  // elements between V components
     const int64_t row_el = (int64_t)W * Cpad;
     for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
         const IDX t = i / groups;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restr
                 }
             }
         }
-        const int64_t base = (int64_t)t * Cpad + cgi * VC;
+        const int64_t base = (int64_t)t * (tmajor ? 16 * Cpad : Cpad) + cgi * VC;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             float bt[4][VC];  // row a of B^T d, per channel
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(const void* __restr
 
 cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W, int64_t Cpad, int64_t P,
                                   int64_t Q, int ph, int pw, ComputeMode cm, const void* /*x_lo*/, void* V,
-                                  void* V_lo, cudaStream_t st) {
+                                  void* V_lo, int tmajor, cudaStream_t st) {
     const int64_t TH = (P + 1) / 2, TW = (Q + 1) / 2;
     if (N > INT32_MAX || H > INT32_MAX / 2 || W > INT32_MAX / 2 || Cpad > INT32_MAX) return cudaErrorInvalidValue;
     const int64_t total = N * TH * TW * (Cpad / 4);
@@ -444,11 +444,11 @@ cudaError_t launch_winograd_input(const void* x, int64_t N, int64_t H, int64_t W
     const bool small = total < (1LL << 31);
     const int n = (int)N, h = (int)H, w = (int)W, c = (int)Cpad, th = (int)TH, tw = (int)TW;
     if (cm == CM_BF16) {
-        if (small) winograd_input_kernel<true, uint32_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo);
-        else winograd_input_kernel<true, int64_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo);
+        if (small) winograd_input_kernel<true, uint32_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo, tmajor);
+        else winograd_input_kernel<true, int64_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo, tmajor);
     } else {
-        if (small) winograd_input_kernel<false, uint32_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo);
-        else winograd_input_kernel<false, int64_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo);
+        if (small) winograd_input_kernel<false, uint32_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo, tmajor);
+        else winograd_input_kernel<false, int64_t><<<grid, 256, 0, st>>>(x, n, h, w, c, th, tw, ph, pw, cm, V, V_lo, tmajor);
     }
     return cudaGetLastError();
 }

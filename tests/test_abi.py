@@ -165,6 +165,9 @@ def test_workspace_sizes():
     # Winograd: 16 transformed tiles in (V) and out (M: bf16 for bf16 runs, fp32 otherwise)
     T = 64 * 28 * 28
     assert ws((64, 256, 56, 56), 256, 3, "winograd") >= 16 * T * 256 * 2 + 16 * T * 256 * 2
+    # bf16 NHWC outputs with K <= 64 run the fused kernel (M stays in TMEM): V only
+    assert 16 * T * 256 * 2 <= ws((64, 256, 56, 56), 64, 3, "winograd") < 16 * T * 256 * 2 + 16 * T * 64 * 2
+    assert ws((64, 256, 56, 56), 64, 3, "winograd", lout=_lib.NCHW) >= 16 * T * 256 * 2 + 16 * T * 64 * 2
     assert ws((64, 256, 56, 56), 256, 3, "winograd", dtype=_lib.F32) >= 16 * T * 256 * 4 + 16 * T * 256 * 4
     # direct needs no workspace beyond the fp32 weights [Cg][R][S][K padded to 64] and the fp32
     # bias, each region 256-byte aligned: 3*3*3*64*4 = 6912 (already aligned) + 256
