@@ -443,6 +443,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         // 128-byte K-block rows: cp.async gather (16 bytes per lane); narrower rows: TMA gather4
         a.ga_async = (a.row_bytes == 128 && knob("AI3_GATHER_ASYNC", 1)) ? 1 : 0;
         a.ga_pitch = (int)(pl.Cpad * pl.elem);
+        a.ga_off32 = (uint64_t)c.N * c.H * c.W * pl.Cpad * pl.elem < (1ull << 32) ? 1 : 0;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);
     } else if (algo == AI3_ALGO_IMPLICIT_GEMM && c.R == 1 && c.S == 1 && c.sh == 1 && c.sw == 1 && c.ph == 0 &&
                c.pw == 0) {

@@ -219,6 +219,7 @@ struct TcArgs {
     // [N*H*W][ga_pitch bytes] (3xTF32: hi / lo parts)
     int ga_async;
     int ga_pitch;
+    int ga_off32;   // every source row offset (row * ga_pitch + 127) fits 32 bits
     const char* ga_src;
     const char* ga_src_lo;
     // fused Winograd F(2x2,3x3) (wf = 1; batch = 16, block_n = 32, bf16): every CTA group runs

@@ -452,6 +452,26 @@ __device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUt
             __syncwarp();
             const uint32_t sA = s0 + stage * stage_bytes;
             const size_t col = (size_t)cc * 128 + chunk * 16;
+            if (splits == 1 && a.ga_off32) {
+                // one operand part, 32-bit source offsets: ~6 instructions per 16-byte copy
+                const char* src = a.ga_src + (uint32_t)(cc * 128 + chunk * 16);
+                const uint32_t pitch = (uint32_t)a.ga_pitch;
+                const uint32_t d0 = sA + sub_row * 128 + ((chunk ^ sub_row) << 4), d1 = d0 ^ (4u << 4);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < j0 || j >= j1) continue;
+                    const int row = 4 * j + sub_row;
+                    const int reg = j >> 3;  // row >> 5
+                    const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
+                    const int idx = __shfl_sync(0xffffffffu, rv, row & 31);
+                    const uint32_t dst = ((j & 1) ? d1 : d0) + j * 4 * 128;  // row & 7 = 4 (j & 1) + sub_row
+                    cp_async16(dst, src + (uint32_t)(idx < 0 ? 0 : idx) * pitch, idx < 0 ? 0u : 16u);
+                }
+                cp_async_mbar_arrive_noinc(&full[stage]);
+                if (++cc == a.c_chunks) { cc = 0; ++tap; r_cur = r_next; }
+                if (++stage == a.stages) { stage = 0; phase ^= 1; }
+                continue;
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3; this lane: row 4j + sub_row, chunk
                 if (j < j0 || j >= j1) continue;
