@@ -40,7 +40,18 @@ using namespace direct_detail;
 // every staged input element feeds 64 channels).  QG: column groups of 8 pixels per tile
 // row; the tile is (256 / NKG / QG) rows x 8*QG columns, picked per layer so that small
 // feature maps (28x28, 14x14) do not pad to 64-wide tiles.
-template <int KS, bool UNIT, int QG, int NKG>
+// Asynchronous staging (async_pf = 1: NHWC input, Cg and CB multiples of 16 bytes of
+// channels): the raw footprint of the NEXT channel chunk -- pixel rows of cb channels,
+// zero-filled outside the image -- and its weights stream into shared memory with cp.async
+// while the CTA computes the current chunk; the raw chunk is then widened / transposed
+// smem -> smem into the fp32 planes the compute loop reads (one 16-byte piece per step).
+// Measured before (ncu, VGG conv3_2): the synchronous global -> smem staging of every chunk
+// left the FP32 pipe at 62 %.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16u : 0u) : "memory");
+}
+
+template <int KS, bool UNIT, int QG, int NKG, bool ASYNC>
 __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
                                                             int xs_floats) {
     constexpr int TK = 8 * NKG, PT = NT / NKG;  // pixel threads per k group
@@ -71,27 +82,7 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     const int64_t xsW = a.in_nhwc ? a.C : 1;
     const int64_t xbase = (int64_t)n * xsN + (int64_t)g * a.Cg * xsC;
 
-    for (int c0 = 0; c0 < a.Cg; c0 += CB) {
-        const int cb = min(CB, a.Cg - c0);
-        // ---- stage the input footprint (zeros outside the image)
-        // ---- weights [cc][r][s][TK]: contiguous 16-byte pieces of the prepared rows, copied
-        //      asynchronously (cp.async) so they stream in while the footprint is staged
-        {
-            const int nq = cb * R * S * (TK / 4);
-            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
-            for (int i = tid; i < nq; i += NT) {
-                const int row = i / (TK / 4), qd = i % (TK / 4);  // row (cc, r, s), 4-channel piece
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + row * TK + 4 * qd);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
-                             : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
-                            ih0, iw0, cb, FH, FW, FWp, tid);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
+    auto compute_chunk = [&](int cb, const float* xs, const float* ws) {
         for (int cc = 0; cc < cb; ++cc) {
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
@@ -134,7 +125,109 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
                 }
             }
         }
+    };
+
+    if constexpr (ASYNC) {
+        // smem: xs [CB][FH][FWp] fp32 | ws0, ws1 [CB][R][S][TK] | raw [FH][FW][CB] input dtype
+        const int wsz = CB * R * S * TK;
+        auto wsb = [&](int b) { return smem + xs_floats + (b ? wsz : 0); };  // (no runtime-indexed local array)
+        uint8_t* raw = reinterpret_cast<uint8_t*>(smem + xs_floats + 2 * wsz);
+        const int eb = a.bf16 ? 2 : 4, per16 = 16 / eb;  // elements per 16-byte piece
+        const char* xb = reinterpret_cast<const char*>(a.x) + (xbase * eb);
+        auto prefetch = [&](int c0, int buf) {
+            const int cb = min(CB, a.Cg - c0);
+            const int pp = cb / per16;  // pieces per pixel
+            const int total = FH * FW * pp;
+            int pc = tid % pp, pix = tid / pp;
+            const int step_pc = NT % pp, step_pix = NT / pp;
+            int y = pix / FW, xw = pix - (pix / FW) * FW;
+            const int step_y = step_pix / FW, step_x = step_pix - step_y * FW;
+            for (int i = tid; i < total; i += NT) {
+                const int ih = ih0 + y, iw = iw0 + xw;
+                const bool ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                const char* src = ok ? xb + ((int64_t)ih * xsH + (int64_t)iw * xsW + c0 + pc * per16) * eb : xb;
+                cp_async16_zfill((uint32_t)__cvta_generic_to_shared(raw + ((size_t)(y * FW + xw) * cb + pc * per16) * eb),
+                                 src, ok);
+                // advance (pc, xw, y) by NT pieces
+                pc += step_pc;
+                int c = pc >= pp;
+                pc -= c ? pp : 0;
+                xw += step_x + c;
+                c = xw >= FW;
+                xw -= c ? FW : 0;
+                y += step_y + c;
+            }
+            const int nq = cb * R * S * (TK / 4);
+            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+            for (int i = tid; i < nq; i += NT) {
+                const int row = i / (TK / 4), qd = i % (TK / 4);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wsb(buf) + row * TK + 4 * qd);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        prefetch(0, 0);
+        int buf = 0;
+        for (int c0 = 0; c0 < a.Cg; c0 += CB, buf ^= 1) {
+            const int cb = min(CB, a.Cg - c0);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();  // raw chunk + weights landed; the previous chunk's compute is done
+            {   // widen / transpose: raw [FH][FW][cb] -> xs [cb][FH][FWp], one 16-byte piece per step
+                const int pp = cb / per16;
+                const int total = FH * FW * pp;
+                for (int i = tid; i < total; i += NT) {
+                    const int pix = i / pp, pc = i - pix * pp;
+                    const int y = pix / FW, xw = pix - y * FW;
+                    float v[8];
+                    const uint4 u = *reinterpret_cast<const uint4*>(raw + (size_t)i * 16);
+                    if (a.bf16) {
+                        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = __bfloat1622float2(h[e]);
+                            v[2 * e] = f.x; v[2 * e + 1] = f.y;
+                        }
+                    } else {
+                        v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+                        v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+                    }
+                    float* d = smem + ((pc * per16) * FH + y) * FWp + xw;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (e < per16) d[e * FH * FWp] = v[e];
+                }
+            }
+            __syncthreads();  // xs ready; raw free for the next chunk
+            if (c0 + CB < a.Cg) prefetch(c0 + CB, buf ^ 1);
+            compute_chunk(cb, smem, wsb(buf));
+        }
+    } else {
+    for (int c0 = 0; c0 < a.Cg; c0 += CB) {
+        const int cb = min(CB, a.Cg - c0);
+        // ---- stage the input footprint (zeros outside the image)
+        // ---- weights [cc][r][s][TK]: contiguous 16-byte pieces of the prepared rows, copied
+        //      asynchronously (cp.async) so they stream in while the footprint is staged
+        {
+            const int nq = cb * R * S * (TK / 4);
+            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+            for (int i = tid; i < nq; i += NT) {
+                const int row = i / (TK / 4), qd = i % (TK / 4);  // row (cc, r, s), 4-channel piece
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + row * TK + 4 * qd);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
+                            ih0, iw0, cb, FH, FW, FWp, tid);
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
+        compute_chunk(cb, xs, ws);
+        __syncthreads();
+    }
     }
 
     // ---- epilogue: bias once at the end, optional ReLU, cast, store
@@ -170,16 +263,22 @@ cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     // 16-byte aligned rows; unit-stride row segments read up to 3 floats past FW (never used)
     int FWp = (FW + 3 + 3) / 4 * 4;
     if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
-    const int per_c = (FH * FWp + a.R * a.S * TK) * 4;
     static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (dev knob AI3_DIRECT_KB)
         const int kb = knob("AI3_DIRECT_KB", 48);
         return (kb >= 8 && kb <= 100 ? kb : 48) * 1024;
     }();
-    int CB = budget / per_c;
-    if (CB < 1) CB = 1;
+    // asynchronous staging (see the kernel): NHWC input whose channel chunks are whole 16-byte pieces
+    const int eb = a.bf16 ? 2 : 4, per16 = 16 / eb;
+    const int async_pf = a.in_nhwc && (a.C * eb) % 16 == 0 && a.Cg % per16 == 0 &&
+                         (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && knob("AI3_DIRECT_ASYNC", 1) != 0;
+    const int per_c = async_pf ? FH * FWp * 4 + 2 * a.R * a.S * TK * 4 + FH * FW * eb : (FH * FWp + a.R * a.S * TK) * 4;
+    int CB = (async_pf ? budget * 4 / 3 : budget) / per_c;
+    if (async_pf) CB = CB / per16 * per16;
+    if (CB < (async_pf ? per16 : 1)) CB = async_pf ? per16 : 1;
     if (CB > a.Cg) CB = a.Cg;
     const int xs_floats = (CB * FH * FWp + 3) / 4 * 4;
-    const size_t smem = (size_t)xs_floats * 4 + (size_t)CB * a.R * a.S * TK * 4;
+    const size_t smem = (size_t)xs_floats * 4 + (size_t)(async_pf ? 2 : 1) * CB * a.R * a.S * TK * 4 +
+                        (async_pf ? (size_t)CB * FH * FW * eb : 0);
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
     dim3 grid(tiles, (unsigned)((a.Kg + TK - 1) / TK), (unsigned)(a.N * a.G));
@@ -189,16 +288,21 @@ cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
         kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp, xs_floats);
     };
     const bool sq = a.R == a.S;
-    if (unit) {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG>);
-        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG, NKG>);
-        else launch(direct_conv_kernel<0, true, QG, NKG>);
+    if (async_pf) {  // NHWC staged asynchronously (stride-1 3x3 / 1x1 or generic)
+        if (unit && sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG, true>);
+        else if (unit && sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG, true>);
+        else if (unit) launch(direct_conv_kernel<0, true, QG, NKG, true>);
+        else launch(direct_conv_kernel<0, false, QG, NKG, true>);
+    } else if (unit) {
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG, false>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG, false>);
+        else if (sq && a.R == 5) launch(direct_conv_kernel<5, true, QG, NKG, false>);
+        else launch(direct_conv_kernel<0, true, QG, NKG, false>);
     } else {
-        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG, NKG>);
-        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG, NKG>);
-        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG, NKG>);
-        else launch(direct_conv_kernel<0, false, QG, NKG>);
+        if (sq && a.R == 3) launch(direct_conv_kernel<3, false, QG, NKG, false>);
+        else if (sq && a.R == 1) launch(direct_conv_kernel<1, false, QG, NKG, false>);
+        else if (sq && a.R == 11) launch(direct_conv_kernel<11, false, QG, NKG, false>);
+        else launch(direct_conv_kernel<0, false, QG, NKG, false>);
     }
     return cudaGetLastError();
 }
