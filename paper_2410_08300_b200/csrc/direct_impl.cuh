@@ -60,7 +60,13 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     const int R = KS ? KS : a.R;
     const int S = KS ? KS : a.S;
     const int tid = threadIdx.x;
-    const int qg = tid % QG, pr = (tid % PT) / QG, kg = tid / PT;  // a warp: one k group (broadcast weights)
+    // a warp: one k group (broadcast weights).  QG == 8: a quarter-warp (the 8 lanes of one
+    // 128-bit shared-memory wavefront) covers column groups 0..3 of two adjacent rows instead of
+    // 0..7 of one row: with FWp = 4 (mod 8) its eight 16-byte row loads then hit 32 distinct
+    // banks (0..7 of one row were 2-way conflicted: column groups 8 floats apart)
+    const int l = tid % PT, kg = tid / PT;
+    const int qg = QG == 8 ? ((l & 3) | (((l >> 3) & 1) << 2)) : l % QG;
+    const int pr = QG == 8 ? (((l >> 2) & 1) | ((l >> 4) << 1)) : l / QG;
     const int tiles_q = (int)((a.Q + TQ - 1) / TQ);
     const int p0 = (blockIdx.x / tiles_q) * TP, q0 = (blockIdx.x % tiles_q) * TQ;
     const int k0g = blockIdx.y * TK;
@@ -262,7 +268,7 @@ cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
     // 16-byte aligned rows; unit-stride row segments read up to 3 floats past FW (never used)
     int FWp = (FW + 3 + 3) / 4 * 4;
-    if (FWp % 32 == 0) FWp += 4;  // rows of a warp in different banks
+    if (FWp % 8 == 0) FWp += 4;  // FWp = 4 (mod 8): a quarter-warp's two rows interleave their banks
     static const int budget = [] {  // bytes of staged footprint + weights per channel chunk (dev knob AI3_DIRECT_KB)
         const int kb = knob("AI3_DIRECT_KB", 48);
         return (kb >= 8 && kb <= 100 ? kb : 48) * 1024;
