@@ -440,8 +440,10 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         a.c_chunks = (int)(pl.Cpad * pl.elem / a.row_bytes);
         a.num_kb = (int)(c.R * c.S * a.c_chunks);
         a.gather_rows = (int)pl.idx_rows;
-        // 128-byte K-block rows: cp.async gather (16 bytes per lane); narrower rows: TMA gather4
-        a.ga_async = (a.row_bytes == 128 && knob("AI3_GATHER_ASYNC", 1)) ? 1 : 0;
+        // cp.async gather (16 bytes per lane, any K-block row width); the dev knob
+        // AI3_GATHER_ASYNC=0 restores TMA gather4 (measured ~1 per 87 cycles per SM: VGG conv1_1
+        // with 32-byte rows took 2.4 ms)
+        a.ga_async = knob("AI3_GATHER_ASYNC", 1) ? 1 : 0;
         a.ga_pitch = (int)(pl.Cpad * pl.elem);
         a.ga_off32 = (uint64_t)c.N * c.H * c.W * pl.Cpad * pl.elem < (1ull << 32) ? 1 : 0;
         pl.launches = 1 + (pl.need_prep ? 1 : 0);

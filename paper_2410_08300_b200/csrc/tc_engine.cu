@@ -396,31 +396,38 @@ __device__ __forceinline__ void producer_gather(const TcArgs& a, const CUtensorM
     }
 }
 
-// ---------------------------------------------------------------- gather producer, cp.async (one warp)
+// ---------------------------------------------------------------- gather producer, cp.async (three warps)
 // ga_async (single-CTA tiles): the A tile of K-block (tap, chunk) -- 128 table-named rows x
-// 128 bytes -- moves with cp.async: 8 lanes per row (one 16-byte chunk each, its
-// SWIZZLE_128B slot (c ^ row % 8) computed here), 4 rows per warp instruction, zero fill for
-// rows of -1; the B slice still comes by TMA.  Every lane then arms a cp.async.mbarrier
-// arrive on the stage's full barrier, which counts B's transaction bytes plus the 32 lane
-// arrivals, so the producer never waits for its own copies.  The MMA thread fences the
+// 32 / 64 / 128 bytes -- moves with cp.async: one 16-byte chunk per lane, its swizzled slot
+// computed here, zero fill for rows of -1; the B slice still comes by TMA.  Every lane then
+// arms a cp.async.mbarrier arrive on the stage's full barrier, which counts B's transaction
+// bytes plus the lane arrivals of all producer warps, so no producer waits for its copies.  The MMA thread fences the
 // generic -> async proxy after acquiring the barrier (the tensor core reads smem through the
 // async proxy).  (Measured: one TMA gather4 per 4 rows issued ~1 per 87 cycles per SM, so the
 // gather4 producer ran VGG conv3_2 at 0.13 of the tensor rate.)
-// pid: this producer warp's index (0 .. NUM_GA_EXTRA); it copies the 4-row groups
-// [j0, j1) of every A tile, and warp 0 also issues the B tile's TMA load.
+// pid: this producer warp's index (0 .. NUM_GA_EXTRA); it copies its share of every A
+// tile's row groups, and warp 0 also issues the B tile's TMA load.  CPR: 16-byte chunks per
+// K-block row (8, 4, 2 for 128-, 64-, 32-byte rows); a warp instruction copies 32 / CPR rows.
+// Smem slots follow the TMA swizzle of the row width: chunk j of row r lands at
+// r * row_bytes + ((j ^ sw(r)) << 4), sw = r & 7 (128 B), (r >> 1) & 3 (64 B), (r >> 2) & 1 (32 B)
+// -- the swizzle XORs address bits [4, 7) with bits [7, 10).
+template <int CPR>
 __device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUtensorMap& tb0, const CUtensorMap& tb1,
                                                       uint8_t* smem, uint64_t* full, uint64_t* empty, int unit,
                                                       int num_units, int lane, int pid) {
     constexpr int NP = 1 + NUM_GA_EXTRA;
-    const int j0 = pid * 32 / NP, j1 = (pid + 1) * 32 / NP;
+    constexpr int RPI = 32 / CPR, NI = BM / RPI;  // rows per instruction, instructions per tile
+    constexpr int RB = CPR * 16;                  // row bytes
+    const int j0 = pid * NI / NP, j1 = (pid + 1) * NI / NP;
     const int splits = a.cm == CM_3XTF32 ? 2 : 1;
-    const uint32_t a_bytes = BM * 128u, b_bytes = (uint32_t)a.block_n * 128u;
+    const uint32_t a_bytes = BM * RB, b_bytes = (uint32_t)a.block_n * RB;
     const uint32_t stage_bytes = splits * (a_bytes + b_bytes);
     const int kelems = a.row_bytes / (a.cm == CM_BF16 ? 2 : 4);
     const int tiles_per_batch = a.m_tiles * a.n_tiles;
     const uint32_t s0 = smem_u32(smem);
     const int taps = a.num_kb / a.c_chunks;
-    const int sub_row = lane >> 3, chunk = lane & 7;  // row within a 4-row group, 16-byte chunk
+    const int sub_row = lane / CPR, chunk = lane % CPR;  // row within an RPI-row group, 16-byte chunk
+    auto swz = [](int r) { return CPR == 8 ? (r & 7) : (CPR == 4 ? ((r >> 1) & 3) : ((r >> 2) & 1)); };
     // table entries of rows lane, lane + 32, lane + 64, lane + 96 of (tile, tap)
     auto rows_of = [&](int tile, int tap) -> int4 {
         const int m0 = (tile / a.n_tiles) * BM;
@@ -451,44 +458,49 @@ __device__ __forceinline__ void producer_gather_async(const TcArgs& a, const CUt
             }
             __syncwarp();
             const uint32_t sA = s0 + stage * stage_bytes;
-            const size_t col = (size_t)cc * 128 + chunk * 16;
+            const uint32_t colb = (uint32_t)(cc * RB + chunk * 16);
             if (splits == 1 && a.ga_off32) {
                 // one operand part, 32-bit source offsets: ~6 instructions per 16-byte copy
-                const char* src = a.ga_src + (uint32_t)(cc * 128 + chunk * 16);
+                const char* src = a.ga_src + colb;
                 const uint32_t pitch = (uint32_t)a.ga_pitch;
-                const uint32_t d0 = sA + sub_row * 128 + ((chunk ^ sub_row) << 4), d1 = d0 ^ (4u << 4);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < NI; ++j) {
                     if (j < j0 || j >= j1) continue;
-                    const int row = 4 * j + sub_row;
-                    const int reg = j >> 3;  // row >> 5
+                    const int row = RPI * j + sub_row;
+                    const int reg = row >> 5;
                     const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
                     const int idx = __shfl_sync(0xffffffffu, rv, row & 31);
-                    const uint32_t dst = ((j & 1) ? d1 : d0) + j * 4 * 128;  // row & 7 = 4 (j & 1) + sub_row
+                    const uint32_t dst = sA + row * RB + ((chunk ^ swz(row)) << 4);
                     cp_async16(dst, src + (uint32_t)(idx < 0 ? 0 : idx) * pitch, idx < 0 ? 0u : 16u);
                 }
-                cp_async_mbar_arrive_noinc(&full[stage]);
-                if (++cc == a.c_chunks) { cc = 0; ++tap; r_cur = r_next; }
-                if (++stage == a.stages) { stage = 0; phase ^= 1; }
-                continue;
-            }
+            } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {  // rows 4j .. 4j+3; this lane: row 4j + sub_row, chunk
-                if (j < j0 || j >= j1) continue;
-                const int row = 4 * j + sub_row;
-                const int reg = row >> 5;
-                const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
-                const int idx = __shfl_sync(0xffffffffu, rv, row & 31);
-                const uint32_t dst = sA + row * 128 + ((chunk ^ (row & 7)) << 4);
-                const size_t off = (size_t)(idx < 0 ? 0 : idx) * a.ga_pitch + col;
-                cp_async16(dst, a.ga_src + off, idx < 0 ? 0u : 16u);
-                if (splits == 2) cp_async16(dst + a_bytes, a.ga_src_lo + off, idx < 0 ? 0u : 16u);
+                for (int j = 0; j < NI; ++j) {
+                    if (j < j0 || j >= j1) continue;
+                    const int row = RPI * j + sub_row;
+                    const int reg = row >> 5;
+                    const int rv = reg == 0 ? r_cur.x : (reg == 1 ? r_cur.y : (reg == 2 ? r_cur.z : r_cur.w));
+                    const int idx = __shfl_sync(0xffffffffu, rv, row & 31);
+                    const uint32_t dst = sA + row * RB + ((chunk ^ swz(row)) << 4);
+                    const size_t off = (size_t)(idx < 0 ? 0 : idx) * a.ga_pitch + colb;
+                    cp_async16(dst, a.ga_src + off, idx < 0 ? 0u : 16u);
+                    if (splits == 2) cp_async16(dst + a_bytes, a.ga_src_lo + off, idx < 0 ? 0u : 16u);
+                }
             }
             cp_async_mbar_arrive_noinc(&full[stage]);
             if (++cc == a.c_chunks) { cc = 0; ++tap; r_cur = r_next; }
             if (++stage == a.stages) { stage = 0; phase ^= 1; }
         }
     }
+}
+
+// CPR dispatch of the cp.async gather producer (a.row_bytes = 128 / 64 / 32)
+__device__ __forceinline__ void producer_gather_async_any(const TcArgs& a, const CUtensorMap& tb0, const CUtensorMap& tb1,
+                                                          uint8_t* smem, uint64_t* full, uint64_t* empty, int unit,
+                                                          int num_units, int lane, int pid) {
+    if (a.row_bytes == 128) producer_gather_async<8>(a, tb0, tb1, smem, full, empty, unit, num_units, lane, pid);
+    else if (a.row_bytes == 64) producer_gather_async<4>(a, tb0, tb1, smem, full, empty, unit, num_units, lane, pid);
+    else producer_gather_async<2>(a, tb0, tb1, smem, full, empty, unit, num_units, lane, pid);
 }
 
 // ---------------------------------------------------------------- MMA issuer (one thread)
@@ -1260,11 +1272,11 @@ __global__ void __launch_bounds__(NUM_THREADS_GA, 1)
     const int pk = a.promote_kb > 0 ? a.promote_kb : a.num_kb;
 
     if (warp == 0 && a.a_mode == TC_A_GATHER && a.ga_async) {
-        if (CG == 1) producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane, 0);
+        if (CG == 1) producer_gather_async_any(a, tb0, tb1, smem, full, empty, unit, num_units, lane, 0);
         __syncwarp();
     } else if (warp >= 2 + NUM_EPI_WARPS) {  // extra gather producers (launched for ga_async only)
         if (CG == 1 && a.a_mode == TC_A_GATHER && a.ga_async)
-            producer_gather_async(a, tb0, tb1, smem, full, empty, unit, num_units, lane, warp - (1 + NUM_EPI_WARPS));
+            producer_gather_async_any(a, tb0, tb1, smem, full, empty, unit, num_units, lane, warp - (1 + NUM_EPI_WARPS));
         __syncwarp();
     } else if (warp == 0 && a.a_mode == TC_A_GATHER) {
         producer_gather<CG>(a, ta0, ta1, tb0, tb1, smem, full, empty, rank, unit, num_units, lane);
@@ -1723,7 +1735,8 @@ void tc_configure(TcPlan& p, int num_sms) {
         int st = (SMEM_LIMIT - fixed - NUM_EPI_WARPS * nstg * 32 * a.stg_row) / stage_bytes;
         // fused Winograd: a unit streams 16 stages (one per component), so the ring must hold
         // more than one unit's worth of small stages to cover the load latency (conv1_1: 2 KB)
-        const int cap = a.wf ? 32 : 8;
+        // (likewise the cp.async gather: its stages complete at the gather's latency)
+        const int cap = (a.wf || (a.a_mode == TC_A_GATHER && a.ga_async)) ? 32 : 8;
         return st > cap ? cap : st;
     };
     const int base_stages = stages_for(2);
