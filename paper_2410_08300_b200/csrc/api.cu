@@ -288,6 +288,7 @@ struct ai3_plan {
     bool kn_inplace = false;  // kn2row: fp32 NHWC output accumulates in y itself (no workspace)
     int kn_first = -1;        // kn2row: a tap covering every output pixel (runs first, writes), or -1
     bool wf = false;          // winograd: fused output transform in the GEMM epilogue (no M, TcArgs::wf)
+    bool vt = false;          // winograd: tile-major V [T][16][Cpad] (else [16][T][Cpad])
 };
 
 namespace {
@@ -523,6 +524,7 @@ ai3_status layout_plan_inner(ai3_plan& pl, const ConvProblem& c, ai3_algo algo) 
         pl.ws_M = ws;
         if (!pl.wf) ws = align_up(ws + (size_t)16 * T * c.K * m_elem);
         a.wf = pl.wf ? 1 : 0;
+        pl.vt = pl.wf || knob("AI3_WINO_TMAJOR", 0) != 0;
         a.wf_P = (int)c.P;
         a.wf_Q = (int)c.Q;
         a.wf_TH = (int)((c.P + 1) / 2);
@@ -689,7 +691,7 @@ ai3_status encode_a_maps(ai3_plan& pl, const void* src, const void* src_lo) {
         // V[16][T][Cpad], or tile-major V[T][16][Cpad] for the fused kernel (its CTAs read all 16
         // components of one T tile back to back: one tile's rows stay within a few pages)
         const uint64_t dims[3] = {(uint64_t)pl.Cpad, (uint64_t)a.M, 16};
-        const uint64_t str[2] = {(pl.wf ? 16 : 1) * pl.Cpad * e, (pl.wf ? 1 : (uint64_t)a.M) * pl.Cpad * e};
+        const uint64_t str[2] = {(pl.vt ? 16 : 1) * pl.Cpad * e, (pl.vt ? 1 : (uint64_t)a.M) * pl.Cpad * e};
         const uint32_t box[3] = {kel, 128, 1};
         oka = encode_tiled(&pl.ta0, dt, 3, src, dims, str, box, sw);
         if (oka && pl.splits == 2) oka = encode_tiled(&pl.ta1, dt, 3, src_lo, dims, str, box, sw);
@@ -875,7 +877,7 @@ ai3_status execute(ai3_plan& pl, const void* x, void* y, void* ws, size_t ws_byt
         tp.args.out = y;
     } else {
         e = launch_winograd_input(xs, c.N, c.H, c.W, pl.Cpad, c.P, c.Q, c.ph, c.pw, pl.cm, nullptr, w + pl.ws_V,
-                                  w + pl.ws_Vlo, pl.wf ? 1 : 0, st);
+                                  w + pl.ws_Vlo, pl.vt ? 1 : 0, st);
         if (e != cudaSuccess) return cuda_fail(e, "winograd input transform launch");
         if ((s = encode_a_maps(pl, w + pl.ws_V, w + pl.ws_Vlo)) != AI3_OK) return s;
         if (pl.wf) {
