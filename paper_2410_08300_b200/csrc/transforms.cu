@@ -275,6 +275,55 @@ __global__ void __launch_bounds__(256) im2col_rows_kernel(const void* __restrict
     }
 }
 
+// bf16 -> bf16 rows (the bf16 NHWC `gemm` path): a 16-byte group of A is a 16-byte piece of
+// x, copied without conversion.  Each lane issues all UN loads of its groups of a row before
+// the stores (UN registers of 4 words), so a warp has UN * 32 loads in flight instead of one
+// per lane: the one-group-at-a-time loop was latency-bound (VGG conv1_2: 72 groups per row,
+// 9472 resident warps each walking ~340 rows in 3 dependent load -> store rounds: 2.9 TB/s).
+template <int UN>
+__global__ void __launch_bounds__(256) im2col_rows_bf16_kernel(const uint4* __restrict__ x, int64_t N, int C, int H,
+                                                               int W, int P, int Q, int R, int S, int sh, int sw,
+                                                               int ph, int pw, int dh, int dw, int Kp, uint4* A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t M = N * P * Q;
+    const int groups = Kp / 8, cg = C / 8;          // 16-byte groups per A row / per input pixel
+    const int kred_groups = R * S * cg;
+    // this lane's first group (g = lane) as (filter row, filter column, channel group); later
+    // groups of a row step by 32 groups = (dtap taps, dc groups) with carries (no division)
+    const int tap0 = lane / cg, c0 = lane - tap0 * cg, r0 = tap0 / S, s0 = tap0 - r0 * S;
+    const int dtap = 32 / cg, dc = 32 - dtap * cg;
+    for (int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; m < M;
+         m += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t n = m / ((int64_t)P * Q);
+        const int pq = (int)(m - n * P * Q);
+        const int p = pq / Q, q = pq - (pq / Q) * Q;
+        const int ih0 = p * sh - ph, iw0 = q * sw - pw;
+        const uint4* xn = x + n * H * W * cg;
+        uint4* Am = A + m * groups;
+        int r = r0, sx = s0, c = c0;
+        for (int g0 = lane; g0 < groups; g0 += 32 * UN) {
+            uint4 v[UN];
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                const int g = g0 + 32 * u;
+                v[u] = make_uint4(0, 0, 0, 0);
+                if (g < kred_groups) {
+                    const int ih = ih0 + r * dh, iw = iw0 + sx * dw;
+                    if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W) v[u] = __ldg(xn + (ih * W + iw) * cg + c);
+                }
+                c += dc;
+                const int t = dtap + (c >= cg ? 1 : 0);
+                if (c >= cg) c -= cg;
+                sx += t;
+                while (sx >= S) { sx -= S; ++r; }
+            }
+#pragma unroll
+            for (int u = 0; u < UN; ++u)
+                if (g0 + 32 * u < groups) Am[g0 + 32 * u] = v[u];
+        }
+    }
+}
+
 cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t N, int64_t C, int64_t H, int64_t W,
                           int64_t P, int64_t Q, int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int64_t Kp,
                           ComputeMode cm, void* A, void* A_lo, cudaStream_t st) {
@@ -309,7 +358,16 @@ cudaError_t launch_im2col(const void* x, int in_layout, ai3_dtype dtype, int64_t
         const int64_t warps = N * P * Q;
         const int64_t blocks = (warps * 32 + 255) / 256;
         const int grid = (int)(blocks < 148 * 32 ? blocks : 148 * 32);
-        if (dtype == AI3_BF16)
+        if (dtype == AI3_BF16 && cm == CM_BF16 && (int64_t)H * W * C / 8 < (1LL << 31))
+        {
+            auto go = [&](auto kern) {
+                kern<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), N, (int)C, (int)H, (int)W, (int)P,
+                                           (int)Q, R, S, sh, sw, ph, pw, dh, dw, (int)Kp, reinterpret_cast<uint4*>(A));
+            };
+            if (Kp / 8 > 128) go(im2col_rows_bf16_kernel<8>);  // long rows: 8 loads in flight per lane
+            else go(im2col_rows_bf16_kernel<4>);
+        }
+        else if (dtype == AI3_BF16)
             im2col_rows_kernel<true, 8><<<grid, 256, 0, st>>>(x, N, (int)C, (int)H, (int)W, (int)P, (int)Q, R, S, sh,
                                                                sw, ph, pw, dh, dw, (int)Kp, cm, A, A_lo);
         else
