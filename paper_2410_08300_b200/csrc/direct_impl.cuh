@@ -47,9 +47,6 @@ using namespace direct_detail;
 // smem -> smem into the fp32 planes the compute loop reads (one 16-byte piece per step).
 // Measured before (ncu, VGG conv3_2): the synchronous global -> smem staging of every chunk
 // left the FP32 pipe at 62 %.
-__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool ok) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16u : 0u) : "memory");
-}
 
 template <int KS, bool UNIT, int QG, int NKG, bool ASYNC>
 __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
@@ -138,31 +135,11 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
         const int wsz = CB * R * S * TK;
         auto wsb = [&](int b) { return smem + xs_floats + (b ? wsz : 0); };  // (no runtime-indexed local array)
         uint8_t* raw = reinterpret_cast<uint8_t*>(smem + xs_floats + 2 * wsz);
-        const int eb = a.bf16 ? 2 : 4, per16 = 16 / eb;  // elements per 16-byte piece
+        const int eb = a.bf16 ? 2 : 4;
         const char* xb = reinterpret_cast<const char*>(a.x) + (xbase * eb);
         auto prefetch = [&](int c0, int buf) {
             const int cb = min(CB, a.Cg - c0);
-            const int pp = cb / per16;  // pieces per pixel
-            const int total = FH * FW * pp;
-            int pc = tid % pp, pix = tid / pp;
-            const int step_pc = NT % pp, step_pix = NT / pp;
-            int y = pix / FW, xw = pix - (pix / FW) * FW;
-            const int step_y = step_pix / FW, step_x = step_pix - step_y * FW;
-            for (int i = tid; i < total; i += NT) {
-                const int ih = ih0 + y, iw = iw0 + xw;
-                const bool ok = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
-                const char* src = ok ? xb + ((int64_t)ih * xsH + (int64_t)iw * xsW + c0 + pc * per16) * eb : xb;
-                cp_async16_zfill((uint32_t)__cvta_generic_to_shared(raw + ((size_t)(y * FW + xw) * cb + pc * per16) * eb),
-                                 src, ok);
-                // advance (pc, xw, y) by NT pieces
-                pc += step_pc;
-                int c = pc >= pp;
-                pc -= c ? pp : 0;
-                xw += step_x + c;
-                c = xw >= FW;
-                xw -= c ? FW : 0;
-                y += step_y + c;
-            }
+            stage_raw_async<NT>(raw, xb, eb, xsH, xsW, (int)a.H, (int)a.W, ih0, iw0, c0, cb, FH, FW, tid);
             const int nq = cb * R * S * (TK / 4);
             const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
             for (int i = tid; i < nq; i += NT) {
@@ -180,31 +157,7 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
             const int cb = min(CB, a.Cg - c0);
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();  // raw chunk + weights landed; the previous chunk's compute is done
-            {   // widen / transpose: raw [FH][FW][cb] -> xs [cb][FH][FWp], one 16-byte piece per step
-                const int pp = cb / per16;
-                const int total = FH * FW * pp;
-                for (int i = tid; i < total; i += NT) {
-                    const int pix = i / pp, pc = i - pix * pp;
-                    const int y = pix / FW, xw = pix - y * FW;
-                    float v[8];
-                    const uint4 u = *reinterpret_cast<const uint4*>(raw + (size_t)i * 16);
-                    if (a.bf16) {
-                        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 f = __bfloat1622float2(h[e]);
-                            v[2 * e] = f.x; v[2 * e + 1] = f.y;
-                        }
-                    } else {
-                        v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
-                        v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
-                    }
-                    float* d = smem + ((pc * per16) * FH + y) * FWp + xw;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (e < per16) d[e * FH * FWp] = v[e];
-                }
-            }
+            widen_raw<NT>(smem, raw, a.bf16, cb, FH, FW, FWp, tid);  // raw [FH][FW][cb] -> xs [cb][FH][FWp]
             __syncthreads();  // xs ready; raw free for the next chunk
             if (c0 + CB < a.Cg) prefetch(c0 + CB, buf ^ 1);
             compute_chunk(cb, smem, wsb(buf));

@@ -34,7 +34,10 @@ __device__ __forceinline__ float ld_act(const void* p, int64_t i, int bf16) {
 
 // w is the direct layout [G][Cg][R][S][Kgp] (fp32, k fastest): one tap of KT channels is
 // a contiguous 128-byte run, read as eight broadcast float4 loads.
-template <int KS>
+// ASYNC (NHWC input, channel chunks of whole 16-byte pieces): the next chunk's raw footprint
+// and scalars stream in with cp.async while the current chunk computes (stage.cuh; as in
+// direct_impl.cuh), then the raw chunk is widened into the zero-packed planes.
+template <int KS, bool ASYNC>
 __global__ void __launch_bounds__(NT, 2) smm_conv_kernel(const DirectArgs a, int PB, int FH, int FW, int FWp) {
     extern __shared__ float smem[];
     const int R = KS ? KS : a.R;
@@ -62,27 +65,7 @@ __global__ void __launch_bounds__(NT, 2) smm_conv_kernel(const DirectArgs a, int
     const int64_t xsW = a.in_nhwc ? a.C : 1;
     const int64_t xbase = (int64_t)n * xsN + (int64_t)g * a.Cg * xsC;
 
-    for (int c0 = 0; c0 < a.Cg; c0 += PB) {
-        const int pb = min(PB, a.Cg - c0);
-        // ---- zero-packed planes of channels c0 .. c0+pb-1 (padding written as zeros)
-        // ---- the scalars w[k0g .. k0g+KT)[c][r][s]: 16-byte pieces copied asynchronously while
-        //      the planes are staged
-        {
-            const int nq = pb * R * S * (KT / 4);
-            const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
-            for (int i = tid; i < nq; i += NT) {
-                const int row = i / (KT / 4), qd = i % (KT / 4);
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wsm + row * KT + 4 * qd);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                             "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
-                             : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
-                            ih0, iw0, pb, FH, FW, FWp, tid);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
+    auto compute_chunk = [&](int pb, const float* xs, const float* wsm) {
         for (int cc = 0; cc < pb; ++cc) {
             const float* X = xs + cc * plane;
 #pragma unroll
@@ -109,7 +92,54 @@ __global__ void __launch_bounds__(NT, 2) smm_conv_kernel(const DirectArgs a, int
                 }
             }
         }
+    };
+    auto load_scalars = [&](float* dstw, int c0, int pb) {  // w[k0g .. k0g+KT)[c][r][s], 16-byte pieces
+        const int nq = pb * R * S * (KT / 4);
+        const float* wsrc = a.w + ((int64_t)g * a.Cg * R * S + (int64_t)c0 * R * S) * a.Kgp + k0g;
+        for (int i = tid; i < nq; i += NT) {
+            const int row = i / (KT / 4), qd = i % (KT / 4);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(dstw + row * KT + 4 * qd);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(wsrc + (int64_t)row * a.Kgp + 4 * qd)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (ASYNC) {
+        // smem: xs [PB][FH][FWp] | scalars x2 [PB][R][S][KT] | raw [FH][FW][PB] input dtype
+        const int wsz = PB * R * S * KT;
+        auto wsb = [&](int b) { return wsm + (b ? wsz : 0); };
+        uint8_t* raw = reinterpret_cast<uint8_t*>(wsm + 2 * wsz);
+        const int eb = a.bf16 ? 2 : 4;
+        const char* xb = reinterpret_cast<const char*>(a.x) + xbase * eb;
+        auto prefetch = [&](int c0, int buf) {
+            const int pb = min(PB, a.Cg - c0);
+            stage_raw_async<NT>(raw, xb, eb, xsH, xsW, (int)a.H, (int)a.W, ih0, iw0, c0, pb, FH, FW, tid);
+            load_scalars(wsb(buf), c0, pb);
+        };
+        prefetch(0, 0);
+        int buf = 0;
+        for (int c0 = 0; c0 < a.Cg; c0 += PB, buf ^= 1) {
+            const int pb = min(PB, a.Cg - c0);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();  // raw chunk + scalars landed; the previous chunk's compute is done
+            widen_raw<NT>(xs, raw, a.bf16, pb, FH, FW, FWp, tid);  // zero-packed planes (zeros came with the copy)
+            __syncthreads();
+            if (c0 + PB < a.Cg) prefetch(c0 + PB, buf ^ 1);
+            compute_chunk(pb, xs, wsb(buf));
+        }
+    } else {
+    for (int c0 = 0; c0 < a.Cg; c0 += PB) {
+        const int pb = min(PB, a.Cg - c0);
+        // ---- zero-packed planes of channels c0 .. c0+pb-1 (padding written as zeros); the
+        //      scalars copied asynchronously while the planes are staged
+        load_scalars(wsm, c0, pb);
+        stage_footprint<NT>(xs, a.x, a.bf16, a.in_nhwc, xbase + (int64_t)c0 * xsC, xsC, xsH, xsW, (int)a.H, (int)a.W,
+                            ih0, iw0, pb, FH, FW, FWp, tid);
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
+        compute_chunk(pb, xs, wsm);
+        __syncthreads();
+    }
     }
 
     // ---- bias once at the end, cast, store
@@ -141,11 +171,16 @@ cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st) {
     const int FW = (TQ - 1) * a.sw + (a.S - 1) * a.dw + 1;
     int FWp = FW;
     while (FWp % 32 != 1 && FWp % 32 != 17) ++FWp;  // rows pr and pr+8 of a warp in different banks
-    const int per_plane = (FH * FWp + a.R * a.S * KT) * 4;
-    int PB = (48 * 1024) / per_plane;
-    if (PB < 1) PB = 1;
+    const int eb = a.bf16 ? 2 : 4, per16 = 16 / eb;
+    const bool async_pf = a.in_nhwc && (a.C * eb) % 16 == 0 && a.Cg % per16 == 0 &&
+                          (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && knob("AI3_SMM_ASYNC", 1) != 0;
+    const int per_plane = async_pf ? FH * FWp * 4 + 2 * a.R * a.S * KT * 4 + FH * FW * eb
+                                   : (FH * FWp + a.R * a.S * KT) * 4;
+    int PB = (async_pf ? 64 * 1024 : 48 * 1024) / per_plane;
+    if (async_pf) PB = PB / per16 * per16;
+    if (PB < (async_pf ? per16 : 1)) PB = async_pf ? per16 : 1;
     if (PB > a.Cg) PB = a.Cg;
-    const size_t smem = (size_t)PB * per_plane + 16;
+    const size_t smem = (size_t)PB * per_plane + 64;
     if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
     if (a.Kgp % KT) return cudaErrorInvalidValue;
     const int tiles = (int)(((a.P + TP - 1) / TP) * ((a.Q + TQ - 1) / TQ));
@@ -155,10 +190,15 @@ cudaError_t launch_smm(const DirectArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, NT, smem, st>>>(a, PB, FH, FW, FWp);
     };
-    if (a.R == a.S && a.R == 3) launch(smm_conv_kernel<3>);
-    else if (a.R == a.S && a.R == 1) launch(smm_conv_kernel<1>);
-    else if (a.R == a.S && a.R == 5) launch(smm_conv_kernel<5>);
-    else launch(smm_conv_kernel<0>);
+    if (async_pf) {
+        if (a.R == a.S && a.R == 3) launch(smm_conv_kernel<3, true>);
+        else launch(smm_conv_kernel<0, true>);
+    } else {
+        if (a.R == a.S && a.R == 3) launch(smm_conv_kernel<3, false>);
+        else if (a.R == a.S && a.R == 1) launch(smm_conv_kernel<1, false>);
+        else if (a.R == a.S && a.R == 5) launch(smm_conv_kernel<5, false>);
+        else launch(smm_conv_kernel<0, false>);
+    }
     return cudaGetLastError();
 }
 

@@ -51,4 +51,69 @@ __device__ __forceinline__ void stage_footprint(float* xs, const void* x, int bf
     }
 }
 
+// ---- asynchronous staging (NHWC inputs whose channel chunks are whole 16-byte pieces)
+// stage_raw_async: issue cp.async copies of the raw footprint of channels c0 .. c0+cb of one
+// image -- raw[(y * FW + xw) * cb + c] in the input's dtype (eb bytes), zero-filled outside
+// the image (cp.async src-size 0) -- without waiting.  xb: the image's (and group's) first
+// element; xsH, xsW: element strides of a row / a pixel.
+template <int NT>
+__device__ __forceinline__ void stage_raw_async(uint8_t* raw, const char* xb, int eb, int64_t xsH, int64_t xsW,
+                                                int H, int W, int ih0, int iw0, int c0, int cb, int FH, int FW,
+                                                int tid) {
+    const int per16 = 16 / eb;
+    const int pp = cb / per16;  // pieces per pixel
+    const int total = FH * FW * pp;
+    int pc = tid % pp, pix = tid / pp;
+    const int step_pc = NT % pp, step_pix = NT / pp;
+    int y = pix / FW, xw = pix - (pix / FW) * FW;
+    const int step_y = step_pix / FW, step_x = step_pix - step_y * FW;
+    for (int i = tid; i < total; i += NT) {
+        const int ih = ih0 + y, iw = iw0 + xw;
+        const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
+        const char* src = ok ? xb + ((int64_t)ih * xsH + (int64_t)iw * xsW + c0 + pc * per16) * eb : xb;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(raw + ((size_t)(y * FW + xw) * cb + pc * per16) * eb);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16u : 0u)
+                     : "memory");
+        // advance (pc, xw, y) by NT pieces
+        pc += step_pc;
+        int c = pc >= pp;
+        pc -= c ? pp : 0;
+        xw += step_x + c;
+        c = xw >= FW;
+        xw -= c ? FW : 0;
+        y += step_y + c;
+    }
+}
+
+// widen_raw: raw [FH][FW][cb] (bf16 or fp32) -> xs[(cc * FH + y) * FWp + xw] fp32, one 16-byte
+// piece per step (call after the copies landed and a barrier).
+template <int NT>
+__device__ __forceinline__ void widen_raw(float* xs, const uint8_t* raw, int bf16, int cb, int FH, int FW, int FWp,
+                                          int tid) {
+    const int per16 = bf16 ? 8 : 4;
+    const int pp = cb / per16;
+    const int total = FH * FW * pp;
+    for (int i = tid; i < total; i += NT) {
+        const int pix = i / pp, pc = i - pix * pp;
+        const int y = pix / FW, xw = pix - y * FW;
+        float v[8];
+        const uint4 u = *reinterpret_cast<const uint4*>(raw + (size_t)i * 16);
+        if (bf16) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                v[2 * e] = f.x; v[2 * e + 1] = f.y;
+            }
+        } else {
+            v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y);
+            v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+        }
+        float* d = xs + ((pc * per16) * FH + y) * FWp + xw;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (e < per16) d[e * FH * FWp] = v[e];
+    }
+}
+
 }  // namespace ai3
