@@ -7,7 +7,7 @@
 
 namespace ai3 {
 
-template <int QG, int NKG>
+template <int QG, int NKG, int VQ>
 cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st);
 
 namespace {
@@ -89,15 +89,24 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
     // then the tile shape with the least padded area (ties: the widest rows)
     const int nkg = a.Kg > 32 ? 8 : 4;
     const int pt = NT / nkg;
-    int best = 8;
+    // 7-pixel column groups (VQ = 7) for stride-1 3x3 NHWC layers staged asynchronously
+    const int eb = a.bf16 ? 2 : 4;
+    const bool vq7_ok = a.in_nhwc && a.sh == 1 && a.sw == 1 && a.dh == 1 && a.dw == 1 && a.R == 3 && a.S == 3 &&
+                        (a.C * eb) % 16 == 0 && a.Cg % (16 / eb) == 0 &&
+                        (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && knob("AI3_DIRECT_ASYNC", 1) != 0 &&
+                        knob("AI3_DIRECT_VQ7", 1) != 0;
+    int best = 8, best_vq = 8;
     long long best_area = -1;
-    for (int qg : {8, 4, 2}) {
-        const long long tq = 8 * qg, tp = pt / qg;
-        const long long area = ((a.P + tp - 1) / tp) * tp * ((a.Q + tq - 1) / tq) * tq;
-        if (best_area < 0 || area < best_area) { best = qg; best_area = area; }
+    for (int vq : {8, 7}) {
+        if (vq == 7 && !vq7_ok) continue;
+        for (int qg : {8, 4, 2}) {
+            const long long tq = vq * qg, tp = pt / qg;
+            const long long area = ((a.P + tp - 1) / tp) * tp * ((a.Q + tq - 1) / tq) * tq;
+            if (best_area < 0 || area < best_area) { best = qg; best_vq = vq; best_area = area; }
+        }
     }
     {
-        const long long tq = 8 * best, tp = pt / best;
+        const long long tq = best_vq * best, tp = pt / best;
         const long long ctas = ((a.P + tp - 1) / tp) * ((a.Q + tq - 1) / tq) * ((a.Kg + 8 * nkg - 1) / (8 * nkg)) *
                                a.N * a.G;
         const long long outs = a.N * a.K * a.P * a.Q;
@@ -112,14 +121,24 @@ cudaError_t launch_direct(const DirectArgs& a, cudaStream_t st) {
             return cudaGetLastError();
         }
     }
-    if (nkg == 8) {
-        if (best == 8) return launch_direct_qg<8, 8>(a, st);
-        if (best == 4) return launch_direct_qg<4, 8>(a, st);
-        return launch_direct_qg<2, 8>(a, st);
+    if (best_vq == 7) {
+        if (nkg == 8) {
+            if (best == 8) return launch_direct_qg<8, 8, 7>(a, st);
+            if (best == 4) return launch_direct_qg<4, 8, 7>(a, st);
+            return launch_direct_qg<2, 8, 7>(a, st);
+        }
+        if (best == 8) return launch_direct_qg<8, 4, 7>(a, st);
+        if (best == 4) return launch_direct_qg<4, 4, 7>(a, st);
+        return launch_direct_qg<2, 4, 7>(a, st);
     }
-    if (best == 8) return launch_direct_qg<8, 4>(a, st);
-    if (best == 4) return launch_direct_qg<4, 4>(a, st);
-    return launch_direct_qg<2, 4>(a, st);
+    if (nkg == 8) {
+        if (best == 8) return launch_direct_qg<8, 8, 8>(a, st);
+        if (best == 4) return launch_direct_qg<4, 8, 8>(a, st);
+        return launch_direct_qg<2, 8, 8>(a, st);
+    }
+    if (best == 8) return launch_direct_qg<8, 4, 8>(a, st);
+    if (best == 4) return launch_direct_qg<4, 4, 8>(a, st);
+    return launch_direct_qg<2, 4, 8>(a, st);
 }
 
 }  // namespace ai3

@@ -26,7 +26,7 @@
 namespace ai3 {
 
 namespace direct_detail {
-constexpr int NT = 256, VQ = 8;
+constexpr int NT = 256;
 
 __device__ __forceinline__ float ldx(const void* p, int64_t i, int bf16) {
     return bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]) : reinterpret_cast<const float*>(p)[i];
@@ -48,7 +48,10 @@ using namespace direct_detail;
 // Measured before (ncu, VGG conv3_2): the synchronous global -> smem staging of every chunk
 // left the FP32 pipe at 62 %.
 
-template <int KS, bool UNIT, int QG, int NKG, bool ASYNC>
+// VQ: output pixels per thread along a row (8; or 7 for stride-1 3x3 NHWC layers whose width
+// 7 * QG tiles exactly -- VGG's 224 / 112 / 56 / 28 / 14 -- where 8-wide column groups padded
+// every tile row by 12.5-23 %; the 9-float row segment is then read with scalar loads).
+template <int KS, bool UNIT, int QG, int NKG, bool ASYNC, int VQ = 8>
 __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, int CB, int FH, int FW, int FWp,
                                                             int xs_floats) {
     constexpr int TK = 8 * NKG, PT = NT / NKG;  // pixel threads per k group
@@ -96,10 +99,15 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
                     // qg * VQ % 4 == 0) and slid across the S filter columns in registers
                     constexpr int NSEG = (VQ + (KS ? KS : 1) - 1 + 3) / 4;
                     float xr[NSEG * 4];
+                    if constexpr (VQ % 4 == 0) {
 #pragma unroll
-                    for (int v = 0; v < NSEG; ++v) {
-                        const float4 t = *reinterpret_cast<const float4*>(xrow + 4 * v);
-                        xr[4 * v] = t.x; xr[4 * v + 1] = t.y; xr[4 * v + 2] = t.z; xr[4 * v + 3] = t.w;
+                        for (int v = 0; v < NSEG; ++v) {
+                            const float4 t = *reinterpret_cast<const float4*>(xrow + 4 * v);
+                            xr[4 * v] = t.x; xr[4 * v + 1] = t.y; xr[4 * v + 2] = t.z; xr[4 * v + 3] = t.w;
+                        }
+                    } else {  // qg * VQ is not 16-byte aligned: scalar loads of the VQ + S - 1 used floats
+#pragma unroll
+                        for (int v = 0; v < VQ + (KS ? KS : 1) - 1; ++v) xr[v] = xrow[v];
                     }
 #pragma unroll
                     for (int ss = 0; ss < S; ++ss) {
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(NT, 2) direct_conv_kernel(const DirectArgs a, 
     }
 }
 
-template <int QG, int NKG>
+template <int QG, int NKG, int VQ>
 cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
     constexpr int TK = 8 * NKG, TQ = VQ * QG, TP = NT / NKG / QG;
     const bool unit = a.sw == 1 && a.dw == 1;
@@ -247,6 +255,11 @@ cudaError_t launch_direct_qg(const DirectArgs& a, cudaStream_t st) {
         kern<<<grid, NT, smem, st>>>(a, CB, FH, FW, FWp, xs_floats);
     };
     const bool sq = a.R == a.S;
+    if constexpr (VQ != 8) {  // 7-pixel rows: stride-1 3x3 NHWC with asynchronous staging only
+        if (!(async_pf && unit && sq && a.R == 3)) return cudaErrorInvalidConfiguration;
+        launch(direct_conv_kernel<3, true, QG, NKG, true, VQ>);
+        return cudaGetLastError();
+    }
     if (async_pf) {  // NHWC staged asynchronously (stride-1 3x3 / 1x1 or generic)
         if (unit && sq && a.R == 3) launch(direct_conv_kernel<3, true, QG, NKG, true>);
         else if (unit && sq && a.R == 1) launch(direct_conv_kernel<1, true, QG, NKG, true>);

@@ -3,6 +3,8 @@
 #include "direct_impl.cuh"
 
 namespace ai3 {
-template cudaError_t launch_direct_qg<2, 8>(const DirectArgs& a, cudaStream_t st);
-template cudaError_t launch_direct_qg<2, 4>(const DirectArgs& a, cudaStream_t st);
+template cudaError_t launch_direct_qg<2, 8, 8>(const DirectArgs& a, cudaStream_t st);
+template cudaError_t launch_direct_qg<2, 8, 7>(const DirectArgs& a, cudaStream_t st);
+template cudaError_t launch_direct_qg<2, 4, 8>(const DirectArgs& a, cudaStream_t st);
+template cudaError_t launch_direct_qg<2, 4, 7>(const DirectArgs& a, cudaStream_t st);
 }  // namespace ai3
